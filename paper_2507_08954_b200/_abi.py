@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
+ABI_VERSION = 1
 GFQ_OK, GFQ_EINVAL, GFQ_ERUNTIME, GFQ_ECUDA, GFQ_ENOMEM = 0, 1, 2, 3, 4
 
 POLICY_MQFQ, POLICY_FCFS, POLICY_BATCH, POLICY_SJF, POLICY_FCFS_NAIVE = 0, 1, 2, 3, 4

@@ -1,0 +1,842 @@
+// gfq_engine.cu — kernels and the C ABI (include/gfq.h) of libgfq.so.
+//
+// Kernels
+//   k_trace_index  trace loader: builds, per uploaded trace, the per-flow
+//                  arrival index (CSR of trace positions grouped by flow, in
+//                  arrival order).  Every policy pops queue heads from these
+//                  FIFO slices (pending(f) = arrivals_f[popped
+//                  : arrived]), replacing the reference's per-queue deques
+//                  (core.py:110, FlowQueue.pending).
+//   k_sim          persistent warp-per-simulation engine (sim_warp.cuh): each
+//                  warp pulls simulations from an atomic work queue (longest
+//                  first), runs the reference's event loop to completion and
+//                  then reduces its own completion stream into the
+//                  per-function summary (metrics.py:63-84,195-226) and the
+//                  log-binned latency histograms, so no second pass over the
+//                  records touches HBM.
+//
+// Host ABI: see include/gfq.h for the contract and the reference interface
+// each entry point replaces.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "sim_warp.cuh"
+
+namespace gfq {
+
+// ----------------------------------------------------------------------------
+// stats reducer (runs in the same warp after the event loop)
+//
+// Per function, in completion order (metrics.py:195-220):
+//   count, mean = sum(lat)/n (builtin Neumaier sum), var = sum((x-mean)**2)/(n-1),
+//   cold % = 100*cold/n;
+// weighted_avg_latency (metrics.py:63-77): per-function naive sums in a dict
+// ordered by first completion, then sum(n*(s/n)) / total;
+// cold_hit_rate (metrics.py:80-84); mean_util (metrics.py:223-226).
+// Lane (f mod 32) owns function f; the completion stream is read 32 records
+// at a time (coalesced) and replayed in order through shuffles.
+__device__ void reduce_stats(WarpSim& w, const Params& p) {
+    const int lane = w.lane;
+    const int nf = w.nf;
+    const long long nrec = w.n_comp;
+    // reuse the flow slices: vt = latency sum (then mean), lex = its Neumaier
+    // compensation, tau = naive sum, iat/larr = variance sum + compensation,
+    // pt = count, ph = cold count, infl = first-completion rank,
+    // head = rank -> flow, done = variance-pass count
+    for (int f = lane; f < nf; f += 32) {
+        w.vt[f] = 0.0; w.lex[f] = 0.0; w.tau[f] = 0.0; w.iat[f] = 0.0; w.larr[f] = 0.0;
+        w.pt[f] = 0; w.ph[f] = 0; w.infl[f] = -1; w.done[f] = 0;
+    }
+    __syncwarp();
+    const double* lat = p.comp_lat + w.roff;
+    const int32_t* meta = p.comp_meta + w.roff;
+    int nfirst = 0;
+    long long colds = 0;
+    const bool want_hist = (p.outputs & GFQ_WANT_HIST) && w.sim->group >= 0;
+    const double hl0 = want_hist ? log(p.hist_lo) : 0.0;
+    const double hscale = want_hist ? (double)p.hist_bins / (log(p.hist_hi) - hl0) : 0.0;
+    const int32_t* hrow = p.hist_row + p.tab_off[w.sim->flowtab];
+    for (long long base = 0; base < nrec; base += 32) {
+        long long k = base + lane;
+        double x = 0.0; int32_t m = 0;
+        if (k < nrec) { x = lat[k]; m = meta[k]; }
+        if (want_hist && k < nrec) {
+            int fn = m & 0x7fffffff;
+            int b = x > 0.0 ? (int)floor((log(x) - hl0) * hscale) : 0;
+            b = max(0, min(p.hist_bins - 1, b));
+            int64_t o = ((int64_t)w.sim->group * p.hist_rows + hrow[fn]) * p.hist_bins + b;
+            atomicAdd(&p.hist[o], 1ull);
+        }
+        int cnt = (int)min(32ll, nrec - base);
+        for (int j = 0; j < cnt; j++) {
+            double xj = __shfl_sync(FULLMASK, x, j);
+            int32_t mj = __shfl_sync(FULLMASK, m, j);
+            int fn = mj & 0x7fffffff;
+            bool cold = mj < 0;
+            bool first = false;
+            if ((fn & 31) == lane) {
+                int c = w.pt[fn];
+                if (c == 0) { first = true; w.vt[fn] = 0.0 + xj; }
+                else {
+                    double sf = w.vt[fn];
+                    double t = sf + xj;
+                    if (fabs(sf) >= fabs(xj)) w.lex[fn] += (sf - t) + xj;
+                    else                      w.lex[fn] += (xj - t) + sf;
+                    w.vt[fn] = t;
+                }
+                w.tau[fn] = w.tau[fn] + xj;
+                w.pt[fn] = c + 1;
+                if (cold) w.ph[fn] += 1;
+                if (first) w.infl[fn] = nfirst;
+            }
+            if (__ballot_sync(FULLMASK, first)) nfirst++;
+            colds += cold ? 1 : 0;
+        }
+    }
+    __syncwarp();
+    // means, then the second (variance) pass
+    for (int f = lane; f < nf; f += 32) {
+        int c = w.pt[f];
+        double sv = w.vt[f], sc = w.lex[f];
+        double s = (c == 0) ? 0.0 : ((sc != 0.0 && isfinite(sc)) ? sv + sc : sv);
+        w.vt[f] = c ? s / (double)c : 0.0;                      // mean
+        if (w.infl[f] >= 0) w.head[w.infl[f]] = f;
+    }
+    __syncwarp();
+    for (long long base = 0; base < nrec; base += 32) {
+        long long k = base + lane;
+        double x = 0.0; int32_t m = 0;
+        if (k < nrec) { x = lat[k]; m = meta[k]; }
+        int cnt = (int)min(32ll, nrec - base);
+        for (int j = 0; j < cnt; j++) {
+            double xj = __shfl_sync(FULLMASK, x, j);
+            int fn = __shfl_sync(FULLMASK, m, j) & 0x7fffffff;
+            if ((fn & 31) == lane) {
+                double dx = xj - w.vt[fn];
+                double v = dx * dx;                      // (x - mean) ** 2
+                int c = w.done[fn];
+                if (c == 0) { w.iat[fn] = 0.0 + v; }
+                else {
+                    double sf = w.iat[fn];
+                    double t = sf + v;
+                    if (fabs(sf) >= fabs(v)) w.larr[fn] += (sf - t) + v;
+                    else                     w.larr[fn] += (v - t) + sf;
+                    w.iat[fn] = t;
+                }
+                w.done[fn] = c + 1;
+            }
+        }
+    }
+    __syncwarp();
+    const int64_t fo = p.sim_foff[w.sid];
+    if (p.outputs & GFQ_WANT_STATS) {
+        for (int f = lane; f < nf; f += 32) {
+            int c = w.pt[f];
+            double vf = w.iat[f], vc = w.larr[f];
+            double vs = (c == 0) ? 0.0 : ((vc != 0.0 && isfinite(vc)) ? vf + vc : vf);
+            p.f_count[fo + f] = c;
+            p.f_mean[fo + f] = w.vt[f];
+            p.f_var[fo + f] = c > 1 ? vs / (double)(c - 1) : 0.0;
+            p.f_cold[fo + f] = c ? 100.0 * (double)w.ph[f] / (double)c : 0.0;
+        }
+    }
+    // weighted_avg_latency: builtin sum over functions in first-completion order
+    PySum num; ps_init(num);
+    for (int r = 0; r < nfirst; r++) {
+        int f = w.head[r];
+        double nn = (double)w.pt[f];
+        ps_add(num, nn * (w.tau[f] / nn));
+    }
+    if (lane == 0) {
+        double* sm = p.summary + (int64_t)w.sid * 3;
+        sm[0] = nrec > 0 ? ps_val(num) / (double)nrec : 0.0;
+        sm[1] = nrec > 0 ? 100.0 * ((double)colds / (double)nrec) : 0.0;
+        sm[2] = w.n_util ? ps_val(w.util_sum) / (double)w.n_util : 0.0;
+    }
+}
+
+__device__ void run_one(const Params& p, unsigned char* base, int lane, int sid) {
+    const Layout& L = p.L;
+    WarpSim w;
+    w.P = &p; w.L = &L; w.lane = lane; w.sid = sid;
+    w.vt = (double*)(base + L.o_vt); w.lex = (double*)(base + L.o_lex);
+    w.tau = (double*)(base + L.o_tau); w.iat = (double*)(base + L.o_iat);
+    w.larr = (double*)(base + L.o_larr);
+    w.pt = (int*)(base + L.o_pt); w.ph = (int*)(base + L.o_ph); w.infl = (int*)(base + L.o_infl);
+    w.head = (int*)(base + L.o_head); w.done = (int*)(base + L.o_done);
+    w.fst = (uint8_t*)(base + L.o_fst);
+    w.ev_t = (double*)(base + L.o_ev_t); w.ev_seq = (uint32_t*)(base + L.o_ev_seq);
+    w.ev_meta = (uint32_t*)(base + L.o_ev_meta);
+    w.dvi = (int*)(base + L.o_dvi); w.dvd = (double*)(base + L.o_dvd);
+    w.smp_t = (double*)(base + L.o_smp_t); w.smp_u = (double*)(base + L.o_smp_u);
+    w.run_i = (int*)(base + L.o_run_i); w.run_d = (double*)(base + L.o_run_d);
+    w.pool_m = (uint32_t*)(base + L.o_pool_m); w.pool_t = (double*)(base + L.o_pool_t);
+    w.cnt = (uint16_t*)(base + L.o_cnt);
+
+    const gfq_sim* sim = p.sims + sid;
+    w.sim = sim;
+    const int t = sim->trace;
+    const int64_t toff = p.trace_off[t];
+    w.n = (int)(p.trace_off[t + 1] - toff);
+    w.nf = p.trace_nf[t];
+    w.arr = p.arrival + toff; w.flw = p.flow + toff;
+    w.foff = p.foff + p.foff_off[t]; w.fpos = p.fpos + toff;
+    const int64_t tb = p.tab_off[sim->flowtab];
+    w.warm = p.warm + tb; w.cold = p.cold + tb; w.mem = p.mem + tb;
+    w.share = p.share + tb; w.weight = p.weight + tb;
+    w.policy = sim->policy;
+    w.scripted = sim->device_model == GFQ_DEVMODEL_SCRIPTED;
+    w.mqfq = sim->policy == GFQ_POLICY_MQFQ;
+    w.fcfs = sim->policy == GFQ_POLICY_FCFS || sim->policy == GFQ_POLICY_FCFS_NAIVE;
+    w.dc = p.dcfg + (w.scripted ? 0 : sim->device_cfg);
+    w.ndev = w.scripted ? 1 : sim->n_devices;
+    w.execs = p.execs;
+    w.T = sim->t_overrun; w.alpha = sim->alpha; w.dttl = sim->default_ttl_s;
+    w.roff = p.sim_roff[sid];
+    w.foffs = p.sim_foff[sid];
+
+    // ---- reset the workspace
+    for (int f = lane; f < w.nf; f += 32) {
+        w.vt[f] = 0.0; w.lex[f] = 0.0; w.tau[f] = 0.0; w.iat[f] = 0.0; w.larr[f] = 0.0;
+        w.pt[f] = 0; w.ph[f] = 0; w.infl[f] = 0; w.head[f] = -1; w.done[f] = 0; w.fst[f] = 0;
+    }
+    for (int i = lane; i < 2 * w.ndev * L.F; i += 32) w.cnt[i] = 0;
+    if (lane < w.ndev) {
+        int d = lane;
+        w.dvi[d * 8 + DV_OUT] = 0;
+        w.dvi[d * 8 + DV_EFFD] = w.scripted ? sim->scripted_d : w.dc[d].d_max;
+        w.dvi[d * 8 + DV_NP] = 0; w.dvi[d * 8 + DV_NRUN] = 0;
+        w.dvi[d * 8 + DV_SHEAD] = 0; w.dvi[d * 8 + DV_SN] = 0;
+        w.dvd[d * 2] = 0.0; w.dvd[d * 2 + 1] = 0.0;
+    }
+    __syncwarp();
+    w.period = 0.0;
+    if (!w.scripted) {                                   // engine.py:80-81
+        w.period = w.dc[0].monitor_period_s;
+        for (int d = 1; d < w.ndev; d++) w.period = pymin(w.period, w.dc[d].monitor_period_s);
+    }
+    w.now = 0.0; w.gvt = 0.0;
+    w.seq = (uint32_t)w.n;
+    w.cursor = 0; w.nev = 0;
+    w.tick_on = false; w.tick_t = 0.0; w.tick_seq = 0;
+    w.pmin_ok = true; w.pmin_t = 0.0; w.pmin_seq = 0; w.pmin_slot = -1;
+    w.tot_pend = 0; w.tot_infl = 0;
+    w.fcfs_head = 0; w.fcfs_infl = 0; w.draining = -1;
+    w.s_att = 0; w.s_out = 0; w.s_exec = 0;
+    w.status = 0; w.any_newly = false;
+    w.n_events = w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
+    ps_init(w.util_sum);
+
+    // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
+    // tick (only when the trace is non-empty) seq n
+    if (w.n > 0 && !w.scripted) w.push(w.period, EV_TICK, 0);
+
+    w.run();
+
+    if (!w.status) reduce_stats(w, p);
+    if (lane == 0) {
+        p.status[sid] = w.status;
+        int64_t* c = p.counters + (int64_t)sid * 4;
+        c[0] = w.n_events; c[1] = w.n_calls; c[2] = w.n_disp; c[3] = w.n_util;
+        p.final_time[sid] = w.now;
+        if (p.outputs & GFQ_WANT_AUDIT) p.backlog_count[sid] = w.n_backlog;
+        if (p.outputs & GFQ_WANT_EVENTS) p.event_count[sid] = w.n_evlog;
+        if ((p.outputs & GFQ_WANT_AUDIT) && !w.status &&
+            (w.n_backlog > p.audit_backlog_cap || w.n_util > p.audit_util_cap))
+            p.status[sid] = GFQ_SIM_OUTPUT_OVERFLOW;
+        if ((p.outputs & GFQ_WANT_EVENTS) && !w.status && w.n_evlog > p.event_log_cap)
+            p.status[sid] = GFQ_SIM_OUTPUT_OVERFLOW;
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_sim(const __grid_constant__ Params p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)warp * p.L.bytes;
+    for (;;) {
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(p.work, 1);
+        idx = __shfl_sync(FULLMASK, idx, 0);
+        if (idx >= p.n_sims) break;
+        run_one(p, base, lane, p.order[idx]);
+    }
+}
+
+// Trace loader: one warp per trace.  Counting sort of trace positions by
+// flow rank, stable (arrival order kept within a flow) via __match_any_sync.
+__global__ void k_trace_index(const int32_t* flow, const int64_t* trace_off, const int32_t* trace_nf,
+                              const int64_t* foff_off, int32_t* foff, int32_t* fpos, int n_traces) {
+    extern __shared__ int cursor[];
+    const int t = blockIdx.x;
+    if (t >= n_traces) return;
+    const int lane = threadIdx.x;
+    const int64_t toff = trace_off[t];
+    const int n = (int)(trace_off[t + 1] - toff);
+    const int nf = trace_nf[t];
+    const int32_t* fl = flow + toff;
+    int32_t* fo = foff + foff_off[t];
+    int32_t* fp = fpos + toff;
+    for (int f = lane; f <= nf; f += 32) cursor[f] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) atomicAdd(&cursor[fl[i]], 1);
+    __syncwarp();
+    if (lane == 0) {
+        int acc = 0;
+        for (int f = 0; f < nf; f++) { int c = cursor[f]; cursor[f] = acc; fo[f] = acc; acc += c; }
+        fo[nf] = acc;
+    }
+    __syncwarp();
+    for (int b = 0; b < n; b += 32) {
+        int i = b + lane;
+        bool act = i < n;
+        unsigned am = __ballot_sync(FULLMASK, act);
+        if (act) {
+            int f = fl[i];
+            unsigned peers = __match_any_sync(am, f);
+            int rank = __popc(peers & ((1u << lane) - 1));
+            int pos = cursor[f] + rank;
+            fp[pos] = i;
+            __syncwarp(am);
+            if (lane == 31 - __clz(peers)) cursor[f] += __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace gfq
+
+// ============================================================================
+// host side
+
+using namespace gfq;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) { g_err = msg; return code; }
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return set_err(GFQ_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap && p) return GFQ_OK;
+        if (p) cudaFree(p);
+        p = nullptr; cap = 0;
+        size_t b = std::max<size_t>(bytes, 16);
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) return set_err(GFQ_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        cap = b;
+        return GFQ_OK;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+    template <class T> T* as() const { return (T*)p; }
+};
+
+}  // namespace
+
+struct gfq_handle {
+    int device = 0;
+    int n_sm = 0;
+    size_t smem_optin = 0;
+    // traces
+    DBuf arrival, flow, trace_off, trace_nf, foff_off, foff, fpos;
+    std::vector<int64_t> h_trace_off;
+    std::vector<int32_t> h_trace_nf;
+    int32_t n_traces = 0;
+    // flow tables
+    DBuf warm, cold, mem, share, weight, hist_row, tab_off;
+    std::vector<int64_t> h_tab_off;
+    std::vector<double> h_mem;
+    int32_t n_tabs = 0;
+    // device configs, scripted execs
+    DBuf dcfg, execs;
+    std::vector<gfq_device_cfg> h_dcfg;
+    int64_t n_execs = 0;
+    // staged batch
+    DBuf sims, order, sim_foff, sim_roff, work;
+    std::vector<gfq_sim> h_sims;
+    std::vector<int64_t> h_sim_foff, h_sim_roff;
+    int32_t n_sims = 0;
+    gfq_launch_cfg cfg{};
+    Layout L{};
+    int wpb = 0, blocks = 0;
+    bool prepared = false;
+    DBuf out[GFQ_OUT_COUNT_];
+    int64_t out_n[GFQ_OUT_COUNT_] = {0};
+    int32_t out_b[GFQ_OUT_COUNT_] = {0};
+    DBuf comp_lat, comp_meta;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t last_stream = nullptr;
+    bool launched = false;
+};
+
+static const int32_t kOutBytes[GFQ_OUT_COUNT_] = {
+    4, 8, 8, 8, 8, 8, 8, 8,   // status counters final summary fcount fmean fvar fcold
+    8, 8, 1, 1, 4, 8,         // rec dispatch complete state device order pure
+    4, 8, 8, 4, 4,            // dsp inv vt gvt qlen infl
+    8, 4, 8, 4, 8,            // util rows/meta, backlog time/meta/count
+    8, 8, 8,                  // event time/meta/count
+    8};                       // hist
+
+extern "C" {
+
+const char* gfq_last_error(void) { return g_err.c_str(); }
+int gfq_abi_version(void) { return GFQ_ABI_VERSION; }
+
+int gfq_create(int device, gfq_handle** out) {
+    if (!out) return set_err(GFQ_EINVAL, "gfq_create: out is NULL");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_err(GFQ_EINVAL, "gfq_create: no such CUDA device");
+    CK(cudaSetDevice(device));
+    int major = 0, minor = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+        return set_err(GFQ_ECUDA, "gfq_create: libgfq.so is built for sm_100a (B200) only");
+    gfq_handle* h = new gfq_handle();
+    h->device = device;
+    CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, device));
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    h->smem_optin = (size_t)optin;
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    *out = h;
+    return GFQ_OK;
+}
+
+int gfq_destroy(gfq_handle* h) {
+    if (!h) return GFQ_OK;
+    cudaSetDevice(h->device);
+    DBuf* all[] = {&h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
+                   &h->fpos, &h->warm, &h->cold, &h->mem, &h->share, &h->weight, &h->hist_row,
+                   &h->tab_off, &h->dcfg, &h->execs, &h->sims, &h->order, &h->sim_foff,
+                   &h->sim_roff, &h->work, &h->comp_lat, &h->comp_meta};
+    for (DBuf* b : all) b->release();
+    for (auto& b : h->out) b.release();
+    for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    delete h;
+    return GFQ_OK;
+}
+
+int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
+                      const int64_t* off, const int32_t* n_flows, int32_t n_traces) {
+    if (!h || n_traces < 0 || (n_traces > 0 && (!off || !n_flows)))
+        return set_err(GFQ_EINVAL, "gfq_upload_traces: bad arguments");
+    CK(cudaSetDevice(h->device));
+    if (off[0] != 0) return set_err(GFQ_EINVAL, "gfq_upload_traces: off[0] must be 0");
+    int64_t total = n_traces ? off[n_traces] : 0;
+    int32_t max_nf = 1;
+    std::vector<int64_t> foff_off(n_traces + 1, 0);
+    for (int t = 0; t < n_traces; t++) {
+        int64_t a = off[t], b = off[t + 1];
+        if (b < a) return set_err(GFQ_EINVAL, "gfq_upload_traces: offsets must be non-decreasing");
+        if (b - a >= (1 << 27)) return set_err(GFQ_EINVAL, "gfq_upload_traces: trace longer than 2^27 arrivals");
+        if (n_flows[t] < 0 || n_flows[t] > 0xffff)
+            return set_err(GFQ_EINVAL, "gfq_upload_traces: n_flows out of range");
+        for (int64_t i = a; i < b; i++) {
+            if (flow[i] < 0 || flow[i] >= n_flows[t])
+                return set_err(GFQ_EINVAL, "gfq_upload_traces: flow id out of range in trace " + std::to_string(t));
+            if (i > a && arrival[i] < arrival[i - 1])   // engine.py:72-73
+                return set_err(GFQ_EINVAL, "trace arrival times must be non-decreasing (trace " +
+                                               std::to_string(t) + ")");
+            if (!(arrival[i] >= 0.0) || !isfinite(arrival[i]))
+                return set_err(GFQ_EINVAL, "gfq_upload_traces: arrival times must be finite and >= 0");
+        }
+        foff_off[t + 1] = foff_off[t] + n_flows[t] + 1;
+        max_nf = std::max(max_nf, n_flows[t]);
+    }
+    int rc;
+    if ((rc = h->arrival.ensure(8 * total)) || (rc = h->flow.ensure(4 * total)) ||
+        (rc = h->fpos.ensure(4 * total)) || (rc = h->trace_off.ensure(8 * (n_traces + 1))) ||
+        (rc = h->trace_nf.ensure(4 * std::max(n_traces, 1))) ||
+        (rc = h->foff_off.ensure(8 * (n_traces + 1))) || (rc = h->foff.ensure(4 * foff_off[n_traces])))
+        return rc;
+    if (total) {
+        CK(cudaMemcpy(h->arrival.p, arrival, 8 * total, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->flow.p, flow, 4 * total, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(h->trace_off.p, off, 8 * (n_traces + 1), cudaMemcpyHostToDevice));
+    if (n_traces) CK(cudaMemcpy(h->trace_nf.p, n_flows, 4 * n_traces, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->foff_off.p, foff_off.data(), 8 * (n_traces + 1), cudaMemcpyHostToDevice));
+    if (n_traces) {
+        size_t sm = 4 * ((size_t)max_nf + 1);
+        if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_trace_index, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_trace_index<<<n_traces, 32, sm>>>(h->flow.as<int32_t>(), h->trace_off.as<int64_t>(),
+                                            h->trace_nf.as<int32_t>(), h->foff_off.as<int64_t>(),
+                                            h->foff.as<int32_t>(), h->fpos.as<int32_t>(), n_traces);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+    }
+    h->h_trace_off.assign(off, off + n_traces + 1);
+    h->h_trace_nf.assign(n_flows, n_flows + n_traces);
+    h->n_traces = n_traces;
+    h->prepared = false;
+    return GFQ_OK;
+}
+
+int gfq_upload_flowtabs(gfq_handle* h, const double* warm_s, const double* cold_s,
+                        const double* mem_mb, const double* compute_share,
+                        const double* weight, const int32_t* hist_row,
+                        const int64_t* off, int32_t n_tabs) {
+    if (!h || n_tabs < 0 || !off) return set_err(GFQ_EINVAL, "gfq_upload_flowtabs: bad arguments");
+    CK(cudaSetDevice(h->device));
+    int64_t total = off[n_tabs];
+    for (int64_t i = 0; i < total; i++) {       // FunctionProfile validation, core.py:41-51
+        if (!(warm_s[i] > 0)) return set_err(GFQ_EINVAL, "warm_exec_s must be > 0");
+        if (!(cold_s[i] >= warm_s[i])) return set_err(GFQ_EINVAL, "cold_exec_s must be >= warm_exec_s");
+        if (!(mem_mb[i] > 0)) return set_err(GFQ_EINVAL, "mem_mb must be > 0");
+        if (!(compute_share[i] > 0 && compute_share[i] <= 1)) return set_err(GFQ_EINVAL, "compute_share must be in (0, 1]");
+        if (!(weight[i] > 0)) return set_err(GFQ_EINVAL, "weight must be > 0");
+    }
+    int rc;
+    if ((rc = h->warm.ensure(8 * total)) || (rc = h->cold.ensure(8 * total)) ||
+        (rc = h->mem.ensure(8 * total)) || (rc = h->share.ensure(8 * total)) ||
+        (rc = h->weight.ensure(8 * total)) || (rc = h->hist_row.ensure(4 * total)) ||
+        (rc = h->tab_off.ensure(8 * (n_tabs + 1))))
+        return rc;
+    if (total) {
+        CK(cudaMemcpy(h->warm.p, warm_s, 8 * total, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->cold.p, cold_s, 8 * total, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->mem.p, mem_mb, 8 * total, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->share.p, compute_share, 8 * total, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->weight.p, weight, 8 * total, cudaMemcpyHostToDevice));
+        if (hist_row) CK(cudaMemcpy(h->hist_row.p, hist_row, 4 * total, cudaMemcpyHostToDevice));
+        else CK(cudaMemset(h->hist_row.p, 0, 4 * total));
+    }
+    CK(cudaMemcpy(h->tab_off.p, off, 8 * (n_tabs + 1), cudaMemcpyHostToDevice));
+    h->h_tab_off.assign(off, off + n_tabs + 1);
+    h->h_mem.assign(mem_mb, mem_mb + total);
+    h->n_tabs = n_tabs;
+    h->prepared = false;
+    return GFQ_OK;
+}
+
+int gfq_upload_device_cfgs(gfq_handle* h, const gfq_device_cfg* cfgs, int32_t n) {
+    if (!h || n < 0 || (n > 0 && !cfgs)) return set_err(GFQ_EINVAL, "gfq_upload_device_cfgs: bad arguments");
+    for (int i = 0; i < n; i++) {               // DeviceConfig validation, device.py:36-48
+        const gfq_device_cfg& c = cfgs[i];
+        if (!(c.util_threshold > 0 && c.util_threshold <= 1)) return set_err(GFQ_EINVAL, "util_threshold must be in (0, 1]");
+        if (c.d_max < 1) return set_err(GFQ_EINVAL, "d_max must be >= 1");
+        if (!(c.mem_capacity_mb > 0) || !(c.pcie_mb_per_s > 0) || !(c.monitor_period_s > 0) || !(c.util_window_s > 0))
+            return set_err(GFQ_EINVAL, "device capacities and periods must be > 0");
+        if (c.pool_max_containers < 1) return set_err(GFQ_EINVAL, "pool_max_containers must be >= 1");
+        if (!(c.interference_beta >= 0)) return set_err(GFQ_EINVAL, "interference_beta must be >= 0");
+    }
+    CK(cudaSetDevice(h->device));
+    int rc = h->dcfg.ensure(sizeof(gfq_device_cfg) * std::max(n, 1));
+    if (rc) return rc;
+    if (n) CK(cudaMemcpy(h->dcfg.p, cfgs, sizeof(gfq_device_cfg) * n, cudaMemcpyHostToDevice));
+    h->h_dcfg.assign(cfgs, cfgs + n);
+    h->prepared = false;
+    return GFQ_OK;
+}
+
+int gfq_upload_execs(gfq_handle* h, const double* execs, int64_t n) {
+    if (!h || n < 0 || (n > 0 && !execs)) return set_err(GFQ_EINVAL, "gfq_upload_execs: bad arguments");
+    CK(cudaSetDevice(h->device));
+    int rc = h->execs.ensure(8 * std::max<int64_t>(n, 1));
+    if (rc) return rc;
+    if (n) CK(cudaMemcpy(h->execs.p, execs, 8 * n, cudaMemcpyHostToDevice));
+    h->n_execs = n;
+    h->prepared = false;
+    return GFQ_OK;
+}
+
+static int alloc_out(gfq_handle* h, int id, int64_t n) {
+    int rc = h->out[id].ensure((size_t)std::max<int64_t>(n, 1) * kOutBytes[id]);
+    if (rc) return rc;
+    h->out_n[id] = n;
+    h->out_b[id] = kOutBytes[id];
+    return GFQ_OK;
+}
+
+int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_launch_cfg* cfg) {
+    if (!h || n_sims < 0 || (n_sims > 0 && !sims) || !cfg) return set_err(GFQ_EINVAL, "gfq_prepare: bad arguments");
+    CK(cudaSetDevice(h->device));
+    h->prepared = false;
+    gfq_launch_cfg c = *cfg;
+    if (c.outputs & GFQ_WANT_DISPATCH) c.outputs |= GFQ_WANT_RECORDS;   // rows read dispatch_s
+    int max_nf = 1, nd = 1, P = 1, R = 1, S = 4, max_n = 0;
+    int64_t flows = 0, recs = 0;
+    std::vector<int64_t> foffs(n_sims + 1, 0), roffs(n_sims + 1, 0);
+    std::vector<double> cost(n_sims);
+    for (int i = 0; i < n_sims; i++) {
+        const gfq_sim& s = sims[i];
+        std::string who = "sim " + std::to_string(i) + ": ";
+        if (s.trace < 0 || s.trace >= h->n_traces) return set_err(GFQ_EINVAL, who + "trace id out of range");
+        if (s.flowtab < 0 || s.flowtab >= h->n_tabs) return set_err(GFQ_EINVAL, who + "flow table id out of range");
+        if (s.policy < 0 || s.policy > GFQ_POLICY_FCFS_NAIVE) return set_err(GFQ_EINVAL, who + "unknown policy");
+        if (!(s.t_overrun >= 0)) return set_err(GFQ_EINVAL, who + "t_overrun must be >= 0");
+        if (!(s.alpha >= 0)) return set_err(GFQ_EINVAL, "alpha must be >= 0");
+        int nf = h->h_trace_nf[s.trace];
+        int64_t n = h->h_trace_off[s.trace + 1] - h->h_trace_off[s.trace];
+        int64_t tabn = h->h_tab_off[s.flowtab + 1] - h->h_tab_off[s.flowtab];
+        if (tabn < nf) return set_err(GFQ_EINVAL, who + "flow table shorter than the trace's flow set");
+        if (s.device_model == GFQ_DEVMODEL_SCRIPTED) {
+            if (s.scripted_d < 1 || s.exec_len < 1 || s.exec_off < 0 || s.exec_off + s.exec_len > h->n_execs)
+                return set_err(GFQ_EINVAL, who + "bad scripted-device parameters");
+            R = std::max(R, s.scripted_d);
+        } else if (s.device_model == GFQ_DEVMODEL_DEVICESET) {
+            if (s.n_devices < 1 || s.n_devices > GFQ_MAX_DEVICES)
+                return set_err(GFQ_EINVAL, who + "n_devices must be in [1, 8]");
+            if (s.device_cfg < 0 || s.device_cfg + s.n_devices > (int)h->h_dcfg.size())
+                return set_err(GFQ_EINVAL, who + "device config range out of bounds");
+            nd = std::max(nd, s.n_devices);
+            double period = h->h_dcfg[s.device_cfg].monitor_period_s;
+            for (int d = 0; d < s.n_devices; d++) period = std::min(period, h->h_dcfg[s.device_cfg + d].monitor_period_s);
+            const int64_t tb = h->h_tab_off[s.flowtab];
+            for (int d = 0; d < s.n_devices; d++) {
+                const gfq_device_cfg& dc = h->h_dcfg[s.device_cfg + d];
+                R = std::max(R, dc.d_max);
+                if (dc.pool_enabled) P = std::max(P, dc.pool_max_containers + 1);
+                S = std::max(S, (int)ceil(dc.util_window_s / period) + 3);
+                for (int f = 0; f < nf; f++)    // the reference never terminates otherwise
+                    if (h->h_mem[tb + f] > dc.mem_capacity_mb)
+                        return set_err(GFQ_EINVAL, who + "a function's mem_mb exceeds the device's mem_capacity_mb");
+            }
+        } else {
+            return set_err(GFQ_EINVAL, who + "unknown device model");
+        }
+        max_nf = std::max(max_nf, nf);
+        max_n = std::max<int>(max_n, (int)n);
+        foffs[i + 1] = foffs[i] + nf;
+        roffs[i + 1] = roffs[i] + n;
+        cost[i] = (double)n * (1.0 + nf / 32.0) * (s.policy == GFQ_POLICY_MQFQ ? 2.0 : 1.0);
+    }
+    flows = foffs[n_sims]; recs = roffs[n_sims];
+    Layout L{};
+    L.F = (max_nf + 31) & ~31;
+    L.ND = nd; L.P = P; L.R = R; L.S = S;
+    L.E = c.event_capacity > 0 ? c.event_capacity : std::max(64, ((2 * max_nf + 2 * R * nd + 32) + 31) & ~31);
+    layout_finish(L);
+    if ((size_t)L.bytes > h->smem_optin)
+        return set_err(GFQ_EINVAL, "gfq_prepare: per-simulation workspace (" + std::to_string(L.bytes) +
+                                       " B) exceeds shared memory; reduce flows/pool/event capacity");
+    int wpb = c.warps_per_block > 0 ? c.warps_per_block : 4;
+    while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
+    size_t smem = (size_t)wpb * L.bytes;
+    CK(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim, wpb * 32, smem));
+    if (per_sm < 1) return set_err(GFQ_EINVAL, "gfq_prepare: kernel does not fit on an SM");
+    int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
+    blocks = std::max(1, std::min(blocks, (n_sims + wpb - 1) / wpb));
+
+    int rc;
+    if ((rc = h->sims.ensure(sizeof(gfq_sim) * std::max(n_sims, 1))) || (rc = h->order.ensure(4 * std::max(n_sims, 1))) ||
+        (rc = h->sim_foff.ensure(8 * (n_sims + 1))) || (rc = h->sim_roff.ensure(8 * (n_sims + 1))) ||
+        (rc = h->work.ensure(16)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
+        (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))))
+        return rc;
+    for (int id = 0; id < GFQ_OUT_COUNT_; id++) h->out_n[id] = 0;
+    if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, 4ll * n_sims)) ||
+        (rc = alloc_out(h, GFQ_OUT_FINAL_TIME, n_sims)) || (rc = alloc_out(h, GFQ_OUT_SUMMARY, 3ll * n_sims)))
+        return rc;
+    if (c.outputs & GFQ_WANT_STATS)
+        for (int id : {GFQ_OUT_FLOW_COUNT, GFQ_OUT_FLOW_MEAN, GFQ_OUT_FLOW_VAR, GFQ_OUT_FLOW_COLD_PCT})
+            if ((rc = alloc_out(h, id, flows))) return rc;
+    if (c.outputs & GFQ_WANT_RECORDS)
+        for (int id : {GFQ_OUT_REC_DISPATCH, GFQ_OUT_REC_COMPLETE, GFQ_OUT_REC_STATE, GFQ_OUT_REC_DEVICE,
+                       GFQ_OUT_REC_ORDER, GFQ_OUT_REC_PURE})
+            if ((rc = alloc_out(h, id, recs))) return rc;
+    if (c.outputs & GFQ_WANT_DISPATCH)
+        for (int id : {GFQ_OUT_DSP_INV, GFQ_OUT_DSP_VT_BEFORE, GFQ_OUT_DSP_GVT, GFQ_OUT_DSP_QLEN, GFQ_OUT_DSP_INFLIGHT})
+            if ((rc = alloc_out(h, id, recs))) return rc;
+    if (c.outputs & GFQ_WANT_AUDIT) {
+        if (c.audit_util_cap <= 0) c.audit_util_cap = 1 << 16;
+        if (c.audit_backlog_cap <= 0) c.audit_backlog_cap = 2 * (int64_t)max_n + 2;
+        if ((rc = alloc_out(h, GFQ_OUT_UTIL_ROWS, (int64_t)n_sims * c.audit_util_cap * 3)) ||
+            (rc = alloc_out(h, GFQ_OUT_UTIL_META, (int64_t)n_sims * c.audit_util_cap * 2)) ||
+            (rc = alloc_out(h, GFQ_OUT_BACKLOG_TIME, (int64_t)n_sims * c.audit_backlog_cap)) ||
+            (rc = alloc_out(h, GFQ_OUT_BACKLOG_META, (int64_t)n_sims * c.audit_backlog_cap)) ||
+            (rc = alloc_out(h, GFQ_OUT_BACKLOG_COUNT, n_sims)))
+            return rc;
+    }
+    if (c.outputs & GFQ_WANT_EVENTS) {
+        if (c.event_log_cap <= 0) c.event_log_cap = 64 * (int64_t)max_n + 1024;
+        if ((rc = alloc_out(h, GFQ_OUT_EVENT_TIME, (int64_t)n_sims * c.event_log_cap)) ||
+            (rc = alloc_out(h, GFQ_OUT_EVENT_META, (int64_t)n_sims * c.event_log_cap)) ||
+            (rc = alloc_out(h, GFQ_OUT_EVENT_COUNT, n_sims)))
+            return rc;
+    }
+    if (c.outputs & GFQ_WANT_HIST) {
+        if (c.hist_groups < 1 || c.hist_rows < 1 || c.hist_bins < 1 || !(c.hist_lo_s > 0) || !(c.hist_hi_s > c.hist_lo_s))
+            return set_err(GFQ_EINVAL, "gfq_prepare: bad histogram parameters");
+        if ((rc = alloc_out(h, GFQ_OUT_HIST, (int64_t)c.hist_groups * c.hist_rows * c.hist_bins))) return rc;
+        for (int i = 0; i < n_sims; i++) if (sims[i].group >= c.hist_groups)
+            return set_err(GFQ_EINVAL, "gfq_prepare: sim group out of range");
+    }
+    // longest-first work order (LPT) for the persistent work queue
+    std::vector<int32_t> order(n_sims);
+    for (int i = 0; i < n_sims; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    if (n_sims) {
+        CK(cudaMemcpy(h->sims.p, sims, sizeof(gfq_sim) * n_sims, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->order.p, order.data(), 4 * n_sims, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(h->sim_foff.p, foffs.data(), 8 * (n_sims + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sim_roff.p, roffs.data(), 8 * (n_sims + 1), cudaMemcpyHostToDevice));
+    h->h_sims.assign(sims, sims + n_sims);
+    h->h_sim_foff = foffs; h->h_sim_roff = roffs;
+    h->n_sims = n_sims;
+    h->cfg = c;
+    h->L = L;
+    h->wpb = wpb;
+    h->blocks = blocks;
+    h->prepared = true;
+    h->launched = false;
+    return GFQ_OK;
+}
+
+int gfq_sim_offsets(gfq_handle* h, int64_t* flow_off, int64_t* rec_off) {
+    if (!h || !h->prepared) return set_err(GFQ_EINVAL, "gfq_sim_offsets: no staged batch");
+    if (flow_off) memcpy(flow_off, h->h_sim_foff.data(), 8 * (h->n_sims + 1));
+    if (rec_off) memcpy(rec_off, h->h_sim_roff.data(), 8 * (h->n_sims + 1));
+    return GFQ_OK;
+}
+
+int gfq_launch(gfq_handle* h, void* stream) {
+    if (!h || !h->prepared) return set_err(GFQ_EINVAL, "gfq_launch: no staged batch");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Params p{};
+    p.sims = h->sims.as<gfq_sim>(); p.order = h->order.as<int32_t>(); p.n_sims = h->n_sims;
+    p.arrival = h->arrival.as<double>(); p.flow = h->flow.as<int32_t>();
+    p.trace_off = h->trace_off.as<int64_t>(); p.trace_nf = h->trace_nf.as<int32_t>();
+    p.foff_off = h->foff_off.as<int64_t>(); p.foff = h->foff.as<int32_t>(); p.fpos = h->fpos.as<int32_t>();
+    p.warm = h->warm.as<double>(); p.cold = h->cold.as<double>(); p.mem = h->mem.as<double>();
+    p.share = h->share.as<double>(); p.weight = h->weight.as<double>();
+    p.hist_row = h->hist_row.as<int32_t>(); p.tab_off = h->tab_off.as<int64_t>();
+    p.dcfg = h->dcfg.as<gfq_device_cfg>(); p.execs = h->execs.as<double>();
+    p.sim_foff = h->sim_foff.as<int64_t>(); p.sim_roff = h->sim_roff.as<int64_t>();
+    p.L = h->L;
+    p.outputs = h->cfg.outputs;
+    p.early_exit = h->cfg.early_exit;
+    p.status = h->out[GFQ_OUT_STATUS].as<int32_t>();
+    p.counters = h->out[GFQ_OUT_COUNTERS].as<int64_t>();
+    p.final_time = h->out[GFQ_OUT_FINAL_TIME].as<double>();
+    p.summary = h->out[GFQ_OUT_SUMMARY].as<double>();
+    p.f_count = h->out[GFQ_OUT_FLOW_COUNT].as<int64_t>();
+    p.f_mean = h->out[GFQ_OUT_FLOW_MEAN].as<double>();
+    p.f_var = h->out[GFQ_OUT_FLOW_VAR].as<double>();
+    p.f_cold = h->out[GFQ_OUT_FLOW_COLD_PCT].as<double>();
+    p.comp_lat = h->comp_lat.as<double>(); p.comp_meta = h->comp_meta.as<int32_t>();
+    p.rec_dispatch = h->out[GFQ_OUT_REC_DISPATCH].as<double>();
+    p.rec_complete = h->out[GFQ_OUT_REC_COMPLETE].as<double>();
+    p.rec_pure = h->out[GFQ_OUT_REC_PURE].as<double>();
+    p.rec_state = h->out[GFQ_OUT_REC_STATE].as<int8_t>();
+    p.rec_device = h->out[GFQ_OUT_REC_DEVICE].as<int8_t>();
+    p.rec_order = h->out[GFQ_OUT_REC_ORDER].as<int32_t>();
+    p.dsp_inv = h->out[GFQ_OUT_DSP_INV].as<int32_t>();
+    p.dsp_vt = h->out[GFQ_OUT_DSP_VT_BEFORE].as<double>();
+    p.dsp_gvt = h->out[GFQ_OUT_DSP_GVT].as<double>();
+    p.dsp_qlen = h->out[GFQ_OUT_DSP_QLEN].as<int32_t>();
+    p.dsp_infl = h->out[GFQ_OUT_DSP_INFLIGHT].as<int32_t>();
+    p.util_rows = h->out[GFQ_OUT_UTIL_ROWS].as<double>();
+    p.util_meta = h->out[GFQ_OUT_UTIL_META].as<int32_t>();
+    p.audit_util_cap = h->cfg.audit_util_cap;
+    p.backlog_time = h->out[GFQ_OUT_BACKLOG_TIME].as<double>();
+    p.backlog_meta = h->out[GFQ_OUT_BACKLOG_META].as<int32_t>();
+    p.backlog_count = h->out[GFQ_OUT_BACKLOG_COUNT].as<int64_t>();
+    p.audit_backlog_cap = h->cfg.audit_backlog_cap;
+    p.event_time = h->out[GFQ_OUT_EVENT_TIME].as<double>();
+    p.event_meta = h->out[GFQ_OUT_EVENT_META].as<int64_t>();
+    p.event_count = h->out[GFQ_OUT_EVENT_COUNT].as<int64_t>();
+    p.event_log_cap = h->cfg.event_log_cap;
+    p.hist = h->out[GFQ_OUT_HIST].as<unsigned long long>();
+    p.hist_rows = h->cfg.hist_rows; p.hist_bins = h->cfg.hist_bins;
+    p.hist_lo = h->cfg.hist_lo_s; p.hist_hi = h->cfg.hist_hi_s;
+    p.work = h->work.as<int32_t>();
+    CK(cudaMemsetAsync(h->work.p, 0, 16, st));
+    if (h->cfg.outputs & GFQ_WANT_HIST)
+        CK(cudaMemsetAsync(h->out[GFQ_OUT_HIST].p, 0, 8 * h->out_n[GFQ_OUT_HIST], st));
+    CK(cudaEventRecord(h->ev[0], st));
+    if (h->n_sims > 0) {
+        size_t smem = (size_t)h->wpb * h->L.bytes;
+        k_sim<<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(h->ev[1], st));
+    CK(cudaEventRecord(h->ev[2], st));
+    h->last_stream = st;
+    h->launched = true;
+    return GFQ_OK;
+}
+
+int gfq_synchronize(gfq_handle* h) {
+    if (!h || !h->launched) return set_err(GFQ_EINVAL, "gfq_synchronize: nothing launched");
+    CK(cudaSetDevice(h->device));
+    CK(cudaEventSynchronize(h->ev[2]));
+    if (h->n_sims == 0) return GFQ_OK;
+    std::vector<int32_t> st(h->n_sims);
+    CK(cudaMemcpy(st.data(), h->out[GFQ_OUT_STATUS].p, 4 * h->n_sims, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < h->n_sims; i++)
+        if (st[i] != GFQ_SIM_OK) {
+            static const char* names[] = {"ok", "dynamic event pool overflow", "utilization-sample buffer overflow",
+                                          "watchdog: event budget exhausted", "event scheduled in the past",
+                                          "output buffer overflow", "container pool / running set overflow",
+                                          "bad simulation state"};
+            return set_err(GFQ_ERUNTIME, "simulation " + std::to_string(i) + " failed: " +
+                                             (st[i] >= 0 && st[i] <= 7 ? names[st[i]] : "unknown"));
+        }
+    return GFQ_OK;
+}
+
+int gfq_last_kernel_ms(gfq_handle* h, float* sim_ms, float* reduce_ms) {
+    if (!h || !h->launched) return set_err(GFQ_EINVAL, "gfq_last_kernel_ms: nothing launched");
+    CK(cudaEventSynchronize(h->ev[2]));
+    float a = 0, b = 0;
+    CK(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+    CK(cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+    if (sim_ms) *sim_ms = a;
+    if (reduce_ms) *reduce_ms = b;
+    return GFQ_OK;
+}
+
+int gfq_output_info(gfq_handle* h, int32_t id, int64_t* n_elems, int32_t* elem_bytes) {
+    if (!h || id < 0 || id >= GFQ_OUT_COUNT_) return set_err(GFQ_EINVAL, "gfq_output_info: bad id");
+    if (n_elems) *n_elems = h->out_n[id];
+    if (elem_bytes) *elem_bytes = kOutBytes[id];
+    return GFQ_OK;
+}
+
+int gfq_output_copy(gfq_handle* h, int32_t id, void* host_dst, int64_t bytes) {
+    if (!h || id < 0 || id >= GFQ_OUT_COUNT_) return set_err(GFQ_EINVAL, "gfq_output_copy: bad id");
+    int64_t have = h->out_n[id] * kOutBytes[id];
+    if (bytes > have) return set_err(GFQ_EINVAL, "gfq_output_copy: request larger than the output");
+    CK(cudaSetDevice(h->device));
+    if (bytes) CK(cudaMemcpy(host_dst, h->out[id].p, bytes, cudaMemcpyDeviceToHost));
+    return GFQ_OK;
+}
+
+int gfq_output_device_ptr(gfq_handle* h, int32_t id, void** dptr) {
+    if (!h || id < 0 || id >= GFQ_OUT_COUNT_ || !dptr) return set_err(GFQ_EINVAL, "gfq_output_device_ptr: bad id");
+    *dptr = h->out_n[id] ? h->out[id].p : nullptr;
+    return GFQ_OK;
+}
+
+int gfq_run(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_launch_cfg* cfg) {
+    int rc = gfq_prepare(h, sims, n_sims, cfg);
+    if (rc) return rc;
+    if ((rc = gfq_launch(h, nullptr))) return rc;
+    return gfq_synchronize(h);
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// gfq_layout.h — shared (host + device) description of the per-simulation
+// shared-memory workspace and the kernel parameter block.
+//
+// One simulation runs per warp.  Its mutable state lives in a private slice
+// of the CTA's dynamic shared memory, laid out structure-of-arrays so that
+// the warp's lane-parallel scans (lane i owns flows i, i+32, ...; pool
+// entries i, i+32, ...; event slots i, i+32, ...) are bank-conflict free.
+// Sizes are per batch (the maxima over the batch's simulations), computed
+// on the host by gfq_layout_make() and mirrored on the device.
+#pragma once
+#include <stdint.h>
+#include "../../include/gfq.h"
+
+namespace gfq {
+
+// flow state bits (per flow, u8)
+enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
+
+// per-device int fields
+enum { DV_OUT = 0, DV_EFFD, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_NI };
+
+// event kinds (engine.py:20-23)
+enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };
+
+struct Layout {
+    int32_t F;      // flow slots (multiple of 32)
+    int32_t E;      // dynamic event slots (completions + keep-alive expiries)
+    int32_t ND;     // modeled devices
+    int32_t P;      // container pool slots per device (pool_max + 1)
+    int32_t R;      // running slots per device (max d_max)
+    int32_t S;      // utilization-sample ring slots per device
+    // byte offsets inside one warp's slice (all 8-byte aligned)
+    int32_t o_vt, o_lex, o_tau, o_iat, o_larr;          // f64[F]
+    int32_t o_pt, o_ph, o_infl, o_head, o_done;          // i32[F]
+    int32_t o_fst;                                       // u8[F]
+    int32_t o_ev_t, o_ev_seq, o_ev_meta;                 // f64[E], u32[E], u32[E]
+    int32_t o_dvi, o_dvd;                                // i32[ND][8], f64[ND][2]
+    int32_t o_smp_t, o_smp_u;                            // f64[ND][S]
+    int32_t o_run_i, o_run_d;                            // i32[ND][R][4], f64[ND][R][2]
+    int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
+    int32_t o_cnt;                                       // u16[ND][2][F]
+    int32_t bytes;                                       // slice size
+};
+
+struct Params {
+    const gfq_sim* sims;
+    const int32_t* order;          // work-queue order of sims (longest first)
+    int32_t n_sims;
+    // traces (CSR) and their per-flow arrival index (built by the loader)
+    const double* arrival;
+    const int32_t* flow;
+    const int64_t* trace_off;      // [n_traces + 1]
+    const int32_t* trace_nf;       // [n_traces]
+    const int64_t* foff_off;       // [n_traces + 1] offsets into foff
+    const int32_t* foff;           // per trace: nf + 1 offsets into fpos (trace-relative)
+    const int32_t* fpos;           // per trace: arrival positions grouped by flow
+    // flow tables (profiles + weights)
+    const double *warm, *cold, *mem, *share, *weight;
+    const int32_t* hist_row;
+    const int64_t* tab_off;
+    const gfq_device_cfg* dcfg;
+    const double* execs;
+    // per-sim output offsets
+    const int64_t* sim_foff;       // flow offset per sim
+    const int64_t* sim_roff;       // record offset per sim
+    Layout L;
+    uint32_t outputs;
+    int32_t early_exit;
+    // outputs
+    int32_t* status;
+    int64_t* counters;             // [sims][4]
+    double* final_time;
+    double* summary;               // [sims][3]
+    int64_t* f_count; double* f_mean; double* f_var; double* f_cold;
+    // completion-order scratch (always): latency and flow|cold<<31
+    double* comp_lat; int32_t* comp_meta;
+    double* rec_dispatch; double* rec_complete; double* rec_pure;
+    int8_t* rec_state; int8_t* rec_device; int32_t* rec_order;
+    int32_t* dsp_inv; double* dsp_vt; double* dsp_gvt; int32_t* dsp_qlen; int32_t* dsp_infl;
+    double* util_rows; int32_t* util_meta; int64_t audit_util_cap;
+    double* backlog_time; int32_t* backlog_meta; int64_t* backlog_count; int64_t audit_backlog_cap;
+    double* event_time; int64_t* event_meta; int64_t* event_count; int64_t event_log_cap;
+    unsigned long long* hist; int32_t hist_rows, hist_bins; double hist_lo, hist_hi;
+    int32_t* work;                 // work-queue counter
+};
+
+inline int32_t align8(int32_t x) { return (x + 7) & ~7; }
+
+inline void layout_finish(Layout& L) {
+    int32_t o = 0;
+    auto take = [&](int32_t bytes) { int32_t r = o; o = align8(o + bytes); return r; };
+    const int32_t F = L.F, E = L.E, ND = L.ND, P = L.P, R = L.R, S = L.S;
+    L.o_vt = take(8 * F); L.o_lex = take(8 * F); L.o_tau = take(8 * F);
+    L.o_iat = take(8 * F); L.o_larr = take(8 * F);
+    L.o_pt = take(4 * F); L.o_ph = take(4 * F); L.o_infl = take(4 * F);
+    L.o_head = take(4 * F); L.o_done = take(4 * F);
+    L.o_fst = take(F);
+    L.o_ev_t = take(8 * E); L.o_ev_seq = take(4 * E); L.o_ev_meta = take(4 * E);
+    L.o_dvi = take(4 * 8 * ND); L.o_dvd = take(8 * 2 * ND);
+    L.o_smp_t = take(8 * ND * S); L.o_smp_u = take(8 * ND * S);
+    L.o_run_i = take(4 * 4 * ND * R); L.o_run_d = take(8 * 2 * ND * R);
+    L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);
+    L.o_cnt = take(2 * 2 * ND * F);
+    L.bytes = o;
+}
+
+}  // namespace gfq

@@ -1,0 +1,429 @@
+"""Python face of the B200 engine: the reference's ``run_simulation`` drop-in
+and the batched sweep API, both over libgfq.so (include/gfq.h).
+
+``run_simulation(trace, profiles, policy, devices, tau_includes_overheads)``
+keeps the reference signature and return type (engine.py:214-218): it
+accepts the reference's own ``Trace`` / ``FunctionProfile`` dict /
+``make_policy`` result / ``DeviceSet`` (or this package's mirrors of them,
+duck-typed on ``.entries``, ``.kind``, ``.cfg`` and each device's ``.cfg``)
+and returns ``SimResult(records, audit)`` with ``InvocationRecord`` rows in
+completion order, ``audit.dispatches`` (the DispatchAudit dispatch trace,
+also appended to ``policy.dispatch_log``), ``audit.backlog``,
+``audit.util`` and ``audit.exec``.
+
+``Engine`` is the batch interface: upload traces / flow tables / device
+configs once, then run thousands of independent simulations per launch
+(the serial ``cmd_sweep`` / ``cmd_compare`` loops, cli.py:67-163, become one
+kernel launch).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._lib import check, lib
+from .core import STATE_BY_CODE
+from .mqfq import DispatchAudit
+from .pack import FlowTable, PackedTrace, flow_table, pack_trace
+
+_OUT_DTYPES = {
+    _abi.OUT_STATUS: np.int32, _abi.OUT_COUNTERS: np.int64, _abi.OUT_FINAL_TIME: np.float64,
+    _abi.OUT_SUMMARY: np.float64, _abi.OUT_FLOW_COUNT: np.int64, _abi.OUT_FLOW_MEAN: np.float64,
+    _abi.OUT_FLOW_VAR: np.float64, _abi.OUT_FLOW_COLD_PCT: np.float64,
+    _abi.OUT_REC_DISPATCH: np.float64, _abi.OUT_REC_COMPLETE: np.float64,
+    _abi.OUT_REC_STATE: np.int8, _abi.OUT_REC_DEVICE: np.int8, _abi.OUT_REC_ORDER: np.int32,
+    _abi.OUT_REC_PURE: np.float64, _abi.OUT_DSP_INV: np.int32,
+    _abi.OUT_DSP_VT_BEFORE: np.float64, _abi.OUT_DSP_GVT: np.float64,
+    _abi.OUT_DSP_QLEN: np.int32, _abi.OUT_DSP_INFLIGHT: np.int32,
+    _abi.OUT_UTIL_ROWS: np.float64, _abi.OUT_UTIL_META: np.int32,
+    _abi.OUT_BACKLOG_TIME: np.float64, _abi.OUT_BACKLOG_META: np.int32,
+    _abi.OUT_BACKLOG_COUNT: np.int64, _abi.OUT_EVENT_TIME: np.float64,
+    _abi.OUT_EVENT_META: np.int64, _abi.OUT_EVENT_COUNT: np.int64, _abi.OUT_HIST: np.uint64,
+}
+
+_POLICY = {"mqfq": _abi.POLICY_MQFQ, "fcfs": _abi.POLICY_FCFS, "batch": _abi.POLICY_BATCH,
+           "sjf": _abi.POLICY_SJF, "fcfs_naive": _abi.POLICY_FCFS_NAIVE}
+
+
+def policy_code(kind) -> int:
+    k = getattr(kind, "value", kind)
+    if k not in _POLICY:
+        raise ValueError(f"unknown policy: {kind}")
+    return _POLICY[k]
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(getattr(stream, "cuda_stream"))
+
+
+class Engine:
+    """One libgfq handle bound to one CUDA device (single logical actor)."""
+
+    def __init__(self, device: int = 0):
+        self._L = lib()
+        h = C.c_void_p()
+        check(self._L.gfq_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+        self._keep = []
+        self.n_sims = 0
+        self._flow_off = None
+        self._rec_off = None
+
+    def close(self) -> None:
+        if self._h:
+            self._L.gfq_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---------------------------------------------------------------- inputs
+    def upload_traces(self, traces) -> None:
+        arrs = [np.ascontiguousarray(t.arrival, dtype=np.float64) for t in traces]
+        flows = [np.ascontiguousarray(t.flow, dtype=np.int32) for t in traces]
+        off = np.zeros(len(traces) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([a.shape[0] for a in arrs])
+        arrival = np.concatenate(arrs) if arrs else np.zeros(0)
+        flow = np.concatenate(flows) if flows else np.zeros(0, np.int32)
+        nf = np.array([t.n_flows for t in traces], dtype=np.int32)
+        arrival = np.ascontiguousarray(arrival, dtype=np.float64)
+        flow = np.ascontiguousarray(flow, dtype=np.int32)
+        check(self._L.gfq_upload_traces(self._h, _ptr(arrival, C.c_double), _ptr(flow, C.c_int32),
+                                        _ptr(off, C.c_int64), _ptr(nf, C.c_int32), len(traces)))
+
+    def upload_flowtabs(self, tabs) -> None:
+        cols = {}
+        for name in ("warm", "cold", "mem", "share", "weight"):
+            cols[name] = np.ascontiguousarray(
+                np.concatenate([getattr(t, name) for t in tabs]) if tabs else np.zeros(0),
+                dtype=np.float64)
+        hist = np.ascontiguousarray(
+            np.concatenate([t.hist_row for t in tabs]) if tabs else np.zeros(0, np.int32),
+            dtype=np.int32)
+        off = np.zeros(len(tabs) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([len(t) for t in tabs])
+        check(self._L.gfq_upload_flowtabs(
+            self._h, _ptr(cols["warm"], C.c_double), _ptr(cols["cold"], C.c_double),
+            _ptr(cols["mem"], C.c_double), _ptr(cols["share"], C.c_double),
+            _ptr(cols["weight"], C.c_double), _ptr(hist, C.c_int32), _ptr(off, C.c_int64),
+            len(tabs)))
+
+    def upload_device_cfgs(self, cfgs) -> None:
+        structs = [c if isinstance(c, _abi.DeviceCfg) else _abi.device_cfg_from(c) for c in cfgs]
+        arr = (_abi.DeviceCfg * max(len(structs), 1))(*structs)
+        check(self._L.gfq_upload_device_cfgs(self._h, arr, len(structs)))
+
+    def upload_execs(self, execs) -> None:
+        e = np.ascontiguousarray(execs, dtype=np.float64)
+        check(self._L.gfq_upload_execs(self._h, _ptr(e, C.c_double), int(e.shape[0])))
+
+    # ---------------------------------------------------------------- runs
+    def prepare(self, sims, outputs: int = _abi.WANT_STATS, early_exit: bool = True,
+                **kw) -> None:
+        if isinstance(sims, C.Array):
+            arr, n = sims, len(sims)
+        else:
+            n = len(sims)
+            arr = (_abi.Sim * max(n, 1))(*sims)
+        cfg = _abi.LaunchCfg()
+        cfg.outputs = int(outputs)
+        cfg.early_exit = int(bool(early_exit))
+        for k, v in kw.items():
+            setattr(cfg, k, v)
+        self._keep = [arr]
+        check(self._L.gfq_prepare(self._h, arr, n, C.byref(cfg)))
+        self.n_sims = n
+        fo = np.zeros(n + 1, dtype=np.int64)
+        ro = np.zeros(n + 1, dtype=np.int64)
+        check(self._L.gfq_sim_offsets(self._h, _ptr(fo, C.c_int64), _ptr(ro, C.c_int64)))
+        self._flow_off, self._rec_off = fo, ro
+        self.cfg = cfg
+
+    def launch(self, stream=None) -> None:
+        check(self._L.gfq_launch(self._h, _stream_handle(stream)))
+
+    def synchronize(self) -> None:
+        check(self._L.gfq_synchronize(self._h))
+
+    def kernel_ms(self) -> float:
+        a, b = C.c_float(), C.c_float()
+        check(self._L.gfq_last_kernel_ms(self._h, C.byref(a), C.byref(b)))
+        return float(a.value) + float(b.value)
+
+    def run(self, sims, outputs: int = _abi.WANT_STATS, early_exit: bool = True, **kw):
+        self.prepare(sims, outputs, early_exit, **kw)
+        self.launch()
+        self.synchronize()
+        return BatchResult(self)
+
+    # ---------------------------------------------------------------- outputs
+    def output(self, oid: int) -> np.ndarray:
+        n, b = C.c_int64(), C.c_int32()
+        check(self._L.gfq_output_info(self._h, oid, C.byref(n), C.byref(b)))
+        a = np.empty(n.value, dtype=_OUT_DTYPES[oid])
+        if n.value:
+            check(self._L.gfq_output_copy(self._h, oid, a.ctypes.data_as(C.c_void_p),
+                                          n.value * b.value))
+        return a
+
+    def output_device_ptr(self, oid: int) -> tuple[int, int]:
+        p = C.c_void_p()
+        n, b = C.c_int64(), C.c_int32()
+        check(self._L.gfq_output_device_ptr(self._h, oid, C.byref(p)))
+        check(self._L.gfq_output_info(self._h, oid, C.byref(n), C.byref(b)))
+        return int(p.value or 0), int(n.value)
+
+    @property
+    def flow_off(self):
+        return self._flow_off
+
+    @property
+    def rec_off(self):
+        return self._rec_off
+
+
+class BatchResult:
+    """Host copies of a finished batch's outputs, sliced per simulation."""
+
+    def __init__(self, eng: Engine):
+        self.eng = eng
+        self.n_sims = eng.n_sims
+        self.flow_off = eng.flow_off
+        self.rec_off = eng.rec_off
+        self.cfg = eng.cfg
+        self._cache = {}
+
+    def get(self, oid: int) -> np.ndarray:
+        if oid not in self._cache:
+            self._cache[oid] = self.eng.output(oid)
+        return self._cache[oid]
+
+    @property
+    def status(self):
+        return self.get(_abi.OUT_STATUS)
+
+    @property
+    def counters(self):
+        return self.get(_abi.OUT_COUNTERS).reshape(-1, 4)
+
+    @property
+    def summary(self):
+        return self.get(_abi.OUT_SUMMARY).reshape(-1, 3)
+
+    def dispatches_total(self) -> int:
+        return int(self.counters[:, 2].sum())
+
+    def flow_stats(self, i: int) -> dict:
+        a, b = int(self.flow_off[i]), int(self.flow_off[i + 1])
+        return {"count": self.get(_abi.OUT_FLOW_COUNT)[a:b],
+                "mean": self.get(_abi.OUT_FLOW_MEAN)[a:b],
+                "var": self.get(_abi.OUT_FLOW_VAR)[a:b],
+                "cold_pct": self.get(_abi.OUT_FLOW_COLD_PCT)[a:b]}
+
+    def records(self, i: int) -> dict:
+        """Per-invocation arrays by trace position, plus completion order."""
+        a, b = int(self.rec_off[i]), int(self.rec_off[i + 1])
+        n_done = int(self.counters[i, 2])
+        order = self.get(_abi.OUT_REC_ORDER)[a:b]
+        return {"dispatch": self.get(_abi.OUT_REC_DISPATCH)[a:b],
+                "complete": self.get(_abi.OUT_REC_COMPLETE)[a:b],
+                "state": self.get(_abi.OUT_REC_STATE)[a:b],
+                "device": self.get(_abi.OUT_REC_DEVICE)[a:b],
+                "pure": self.get(_abi.OUT_REC_PURE)[a:b],
+                "order": order, "n": n_done}
+
+    def completion_order(self, i: int) -> np.ndarray:
+        """Trace positions in completion order (every arrival completes in a
+        finished simulation, SPEC: #records == #arrivals)."""
+        order = self.records(i)["order"].astype(np.int64)
+        pos = np.empty(order.shape[0], dtype=np.int64)
+        pos[order] = np.arange(order.shape[0])
+        return pos
+
+    def dispatch_rows(self, i: int) -> dict:
+        a = int(self.rec_off[i])
+        k = int(self.counters[i, 2])
+        return {"inv": self.get(_abi.OUT_DSP_INV)[a:a + k],
+                "vt_before": self.get(_abi.OUT_DSP_VT_BEFORE)[a:a + k],
+                "gvt": self.get(_abi.OUT_DSP_GVT)[a:a + k],
+                "qlen": self.get(_abi.OUT_DSP_QLEN)[a:a + k],
+                "inflight": self.get(_abi.OUT_DSP_INFLIGHT)[a:a + k]}
+
+    def _cap(self, oid: int, per: int) -> int:
+        return int(self.get(oid).shape[0]) // (per * max(self.n_sims, 1))
+
+    def util_rows(self, i: int):
+        cap = self._cap(_abi.OUT_UTIL_META, 2)
+        k = min(int(self.counters[i, 3]), cap)
+        rows = self.get(_abi.OUT_UTIL_ROWS).reshape(-1, cap, 3)[i, :k]
+        meta = self.get(_abi.OUT_UTIL_META).reshape(-1, cap, 2)[i, :k]
+        return rows, meta
+
+    def backlog_rows(self, i: int):
+        cap = self._cap(_abi.OUT_BACKLOG_META, 1)
+        k = min(int(self.get(_abi.OUT_BACKLOG_COUNT)[i]), cap)
+        t = self.get(_abi.OUT_BACKLOG_TIME).reshape(-1, cap)[i, :k]
+        m = self.get(_abi.OUT_BACKLOG_META).reshape(-1, cap)[i, :k]
+        return t, m
+
+    def event_rows(self, i: int):
+        cap = self._cap(_abi.OUT_EVENT_META, 1)
+        k = min(int(self.get(_abi.OUT_EVENT_COUNT)[i]), cap)
+        t = self.get(_abi.OUT_EVENT_TIME).reshape(-1, cap)[i, :k]
+        m = self.get(_abi.OUT_EVENT_META).reshape(-1, cap)[i, :k]
+        return t, m
+
+
+# ----------------------------------------------------------------------------
+# reference-shaped results (metrics.py:18-39, engine.py:26-43)
+
+@dataclass
+class InvocationRecord:
+    function: str
+    arrival_s: float
+    dispatch_s: float
+    complete_s: float
+    start_state: str
+    device: int
+
+    @property
+    def queue_latency_s(self) -> float:
+        return self.dispatch_s - self.arrival_s
+
+    @property
+    def exec_s(self) -> float:
+        return self.complete_s - self.dispatch_s
+
+    @property
+    def latency_s(self) -> float:
+        return self.complete_s - self.arrival_s
+
+
+@dataclass
+class AuditLog:
+    dispatches: list = field(default_factory=list)
+    backlog: list = field(default_factory=list)
+    util: list = field(default_factory=list)
+    exec: list = field(default_factory=list)
+
+
+@dataclass
+class SimResult:
+    records: list
+    audit: AuditLog
+
+
+def sim_params(policy_kind, sched_cfg, n_devices: int, *, trace: int = 0, flowtab: int = 0,
+               device_cfg: int = 0, tau_includes_overheads: bool = False,
+               group: int = -1) -> _abi.Sim:
+    s = _abi.Sim()
+    s.trace, s.flowtab = trace, flowtab
+    s.policy = policy_code(policy_kind)
+    s.device_model = _abi.DEVMODEL_DEVICESET
+    s.n_devices, s.device_cfg = n_devices, device_cfg
+    s.tau_includes_overheads = int(bool(tau_includes_overheads))
+    s.group = group
+    s.t_overrun = float(sched_cfg.t_overrun)
+    s.alpha = float(sched_cfg.alpha)
+    s.default_ttl_s = float(sched_cfg.default_ttl_s)
+    return s
+
+
+_engines: dict[int, Engine] = {}
+
+
+def default_engine(device: int = 0) -> Engine:
+    if device not in _engines:
+        _engines[device] = Engine(device)
+    return _engines[device]
+
+
+def _device_cfgs(devices):
+    cfgs = []
+    for d in devices:
+        cfgs.append(d.cfg if hasattr(d, "cfg") else d)
+    if not cfgs:
+        raise ValueError("at least one device required")
+    return cfgs
+
+
+def run_simulation(trace, profiles, policy, devices, tau_includes_overheads: bool = False,
+                   *, device: int = 0) -> SimResult:
+    """Drop-in for gpufairq.engine.run_simulation (engine.py:214-218), run by
+    the CUDA engine on ``device``."""
+    pt = pack_trace(trace.entries, profiles)
+    cfg = policy.cfg
+    tab = flow_table(pt.names, profiles, getattr(cfg, "weights", None))
+    dcfgs = _device_cfgs(devices)
+    eng = default_engine(device)
+    eng.upload_traces([pt])
+    eng.upload_flowtabs([tab])
+    eng.upload_device_cfgs(dcfgs)
+    sim = sim_params(policy.kind, cfg, len(dcfgs), tau_includes_overheads=tau_includes_overheads)
+    res = eng.run([sim], outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
+                  _abi.WANT_AUDIT, early_exit=True)
+    out = to_sim_result(res, 0, pt)
+    log = getattr(policy, "dispatch_log", None)
+    if isinstance(log, list):
+        log.extend(out.audit.dispatches)
+    return out
+
+
+def to_sim_result(res: BatchResult, i: int, pt: PackedTrace) -> SimResult:
+    names = pt.names
+    rec = res.records(i)
+    k = int(res.counters[i, 2])
+    comp = res.completion_order(i)
+    records = []
+    exe = []
+    for p in comp.tolist():
+        fn = names[int(pt.flow[p])]
+        records.append(InvocationRecord(fn, float(pt.arrival[p]), float(rec["dispatch"][p]),
+                                        float(rec["complete"][p]),
+                                        STATE_BY_CODE[int(rec["state"][p])].value,
+                                        int(rec["device"][p])))
+        exe.append((fn, float(rec["dispatch"][p]), float(rec["complete"][p]),
+                    float(rec["pure"][p])))
+    dr = res.dispatch_rows(i)
+    disp = []
+    for j in range(k):
+        p = int(dr["inv"][j])
+        disp.append(DispatchAudit(now=float(rec["dispatch"][p]), function=names[int(pt.flow[p])],
+                                  vt_before=float(dr["vt_before"][j]),
+                                  global_vt=float(dr["gvt"][j]), queue_len=int(dr["qlen"][j]),
+                                  in_flight=int(dr["inflight"][j]), device=int(rec["device"][p]),
+                                  start_state=STATE_BY_CODE[int(rec["state"][p])].value))
+    audit = AuditLog(dispatches=disp, exec=exe)
+    if res.cfg.outputs & _abi.WANT_AUDIT:
+        rows, meta = res.util_rows(i)
+        audit.util = [(float(r[0]), int(m[0]), float(r[1]), float(r[2]), int(m[1]))
+                      for r, m in zip(rows, meta)]
+        bt, bm = res.backlog_rows(i)
+        audit.backlog = [(float(t), names[int(m) >> 1], bool(int(m) & 1)) for t, m in zip(bt, bm)]
+    return SimResult(records=records, audit=audit)
+
+
+__all__ = ["Engine", "BatchResult", "run_simulation", "sim_params", "SimResult",
+           "InvocationRecord", "AuditLog", "FlowTable", "PackedTrace", "default_engine"]

@@ -1,0 +1,53 @@
+"""Diagnostic runner (GPU box): all golden cases through the engine, per-family
+pass counts, and for the first failures the first differing row vs the oracle."""
+import os
+import sys
+import time
+from collections import Counter, defaultdict
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path[:0] = [os.path.dirname(HERE), HERE, os.path.join(HERE, "golden")]
+
+from cases import all_cases  # noqa: E402
+from golden_check import golden  # noqa: E402
+from gpu_harness import compare_to_golden, first_diff, run_cases  # noqa: E402
+
+from oracle import oracle as orc  # noqa: E402
+
+fams = sys.argv[1:] or None
+cases = [c for c in all_cases() if fams is None or c["name"].split("/")[0] in fams]
+t0 = time.time()
+from paper_2507_08954_b200.engine import Engine  # noqa: E402
+eng = Engine(0)
+outs, res = run_cases(cases, eng, early_exit=False, event_log_cap=65536, audit_util_cap=16384)
+print(f"ran {len(cases)} cases in {time.time() - t0:.1f}s")
+g = golden()
+ok, tot = Counter(), Counter()
+fails = defaultdict(list)
+for c, o in zip(cases, outs):
+    fam = c["name"].split("/")[0]
+    tot[fam] += 1
+    m = compare_to_golden(o, g[c["name"]])
+    if m:
+        fails[fam].append((c, o, m))
+    else:
+        ok[fam] += 1
+for fam in tot:
+    print(f"{fam:12s} {ok[fam]}/{tot[fam]}")
+shown = 0
+for fam, lst in fails.items():
+    for c, o, m in lst[:3]:
+        print("FAIL", c["name"], m, "status", o.get("status"))
+        if o.get("status"):
+            continue
+        ref = orc.run_case(c, want_events=True)
+        for k in ("transcript", "dispatch", "records", "exec", "util", "backlog", "events"):
+            if k in o and k in ref:
+                d = first_diff(o[k], ref[k])
+                if d:
+                    print(f"   {k}: first diff at {d[0]}:\n      gpu={d[1]}\n      ref={d[2]}")
+        for k in ("summary",):
+            if o[k] != ref[k]:
+                print("   summary gpu", o[k], "ref", ref[k])
+        shown += 1
+print("TOTAL", sum(ok.values()), "/", sum(tot.values()))

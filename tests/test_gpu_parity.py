@@ -1,0 +1,71 @@
+"""GPU parity: the CUDA engine against the reference's own outputs.
+
+All 1560 golden cases (tests/golden/reference_golden.json: Appendix-B
+default/medium x 5 policies, the reference's engine scenarios, 400 A1-style
+fuzz instances over every device/scheduler knob, C2/C3/C4 samples, and the
+acceptance suite's 1000 A8 + 100 A11 scripted oracle instances) run as ONE
+batch through libgfq.so.  Dispatch traces, completion records, exec / util /
+backlog audit and the processed-event stream must match the reference's
+fingerprints bit for bit; per-function latency statistics and the run
+summary within 1e-9 relative (north_star).
+"""
+
+from __future__ import annotations
+
+import pytest
+
+from cases import all_cases
+from golden_check import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def engine():
+    from paper_2507_08954_b200.engine import Engine
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def full_run(engine):
+    from gpu_harness import run_cases
+    cases = all_cases()
+    outs, res = run_cases(cases, engine, early_exit=False, event_log_cap=65536,
+                          audit_util_cap=16384)
+    return cases, outs
+
+
+def _report(cases, outs, gold, keys=None):
+    from gpu_harness import compare_to_golden
+    bad = {}
+    for case, out in zip(cases, outs):
+        m = compare_to_golden(out, gold[case["name"]], **({"exact_keys": keys} if keys else {}))
+        if m:
+            bad[case["name"]] = m
+    return bad
+
+
+@pytest.mark.parametrize("family", ["appendix_b", "engine", "fuzz", "c3", "c2", "c4", "a8", "a11"])
+def test_golden_family(full_run, family):
+    cases, outs = full_run
+    sel = [(c, o) for c, o in zip(cases, outs) if c["name"].split("/")[0] == family]
+    bad = _report([c for c, _ in sel], [o for _, o in sel], golden())
+    assert sel
+    assert not bad, f"{len(bad)}/{len(sel)} differ: {dict(list(bad.items())[:6])}"
+
+
+def test_early_exit_is_exact(engine, full_run):
+    """The bench configuration (early exit once only keep-alive rechecks
+    remain) changes no record, dispatch row, audit row or stat."""
+    from gpu_harness import run_cases
+    from paper_2507_08954_b200 import _abi
+    cases, full = full_run
+    outs, _ = run_cases(cases, engine, early_exit=True, audit_util_cap=16384,
+                        outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
+                        _abi.WANT_AUDIT)
+    for c, a, b in zip(cases, outs, full):
+        for k in ("dispatch", "records", "exec", "util", "backlog", "summary", "per_function",
+                  "transcript"):
+            assert a.get(k) == b.get(k), (c["name"], k)
