@@ -1,0 +1,420 @@
+"""bench.py — simulated MQFQ-Sticky dispatch decisions per second on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gfq|reference]
+                    [--workload c3|c2]
+
+A step is one pass of the hot path over one batch: the whole C3 sweep
+(BASELINE configs[2], the configuration the metric's "1/2/4/8 B200" and the
+north-star target are quoted on: 4096 MQFQ-Sticky simulations of a 100-flow
+Azure-shaped Zipf trace, T x alpha x D x 16 seeds) run by one k_sim launch,
+including the in-kernel per-function reducer and latency histograms, plus
+(N > 1) the NCCL all-reduce of the histograms.  Under torchrun each rank
+simulates its own disjoint block of 16 seeds (weak scaling: 4096 sims per
+GPU, no data-path collective).
+
+value   successful dispatches (DispatchAudit rows) summed over all ranks /
+        max-over-ranks device time of the K timed steps, inputs resident in HBM,
+        L2 flushed (256 MiB write) before every step.
+e2e     the same metric through the public Python API with host buffers: trace
+        / flow-table / config / sim-block uploads from pinned memory, launch,
+        and the device->host copy of status, counters, summary and per-function
+        statistics, every step.
+cpu_baseline  the C oracle port (oracle/, the reference algorithm restated in
+        C; ~100x faster than the reference's Python) on one host core, on a
+        bounded random sample of the same sweep.
+--impl reference  the same oracle port on ALL host cores (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated dispatch decisions/s"
+UNIT = "dispatches/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gfq", choices=["gfq", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port) — only bench's cpu_baseline leg and --impl reference
+
+def _oracle_jobs(w, idxs):
+    from oracle import oracle as orc
+    from paper_2507_08954_b200 import _abi
+    jobs = []
+    for i in idxs:
+        s = w.sims[i]
+        tr, tab = w.traces[s.trace], w.tabs[s.flowtab]
+        sim = _abi.Sim.from_buffer_copy(s)
+        dc = w.dcfgs[s.device_cfg: s.device_cfg + s.n_devices]
+        jobs.append((orc, sim, tr, {"warm": tab.warm, "cold": tab.cold, "mem": tab.mem,
+                                     "share": tab.share, "weight": tab.weight},
+                     [_abi.device_cfg_from(d) for d in dc]))
+    return jobs
+
+
+def _oracle_one(job):
+    orc, sim, tr, tab, dc = job
+    r = orc.run_packed(sim, tr.arrival, tr.flow, tr.n_flows, tab, dc, want_audit=False,
+                       want_dispatch=False, want_records=True, want_stats=True)
+    return len(r["rec_inv"])
+
+
+def cpu_sample(w, seconds: float, threads: int, seed: int = 0):
+    """Run random sims of the workload through the oracle for ~`seconds`."""
+    from concurrent.futures import ThreadPoolExecutor
+    rng = random.Random(seed)
+    order = list(range(len(w.sims)))
+    rng.shuffle(order)
+    done_disp, done_sims = 0, 0
+    t0 = time.perf_counter()
+    pos = 0
+    with ThreadPoolExecutor(max_workers=threads) as ex:   # ctypes releases the GIL
+        while time.perf_counter() - t0 < seconds and pos < len(order):
+            chunk = order[pos: pos + 4 * threads]
+            pos += len(chunk)
+            for n in ex.map(_oracle_one, _oracle_jobs(w, chunk)):
+                done_disp += n
+                done_sims += 1
+    dt = time.perf_counter() - t0
+    return done_disp, done_sims, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2507_08954_b200 import sweep
+    import oracle.oracle as orc
+    orc.build()
+    w = sweep.build(args.workload, 0)
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, 60.0 / max(args.steps + args.warmup, 1))
+    for s in range(args.warmup):
+        cpu_sample(w, min(per_step, 2.0), threads, seed=1000 + s)
+    disp, sims, secs = 0, 0, 0.0
+    for s in range(args.steps):
+        d, n, dt = cpu_sample(w, per_step, threads, seed=s)
+        disp += d; sims += n; secs += dt
+    v = disp / secs
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (gen_zipf traces, default profiles)",
+            "config": dict(w.describe, parallelism=f"{threads} host threads"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{sims} random sims of the {args.workload} sweep "
+                                       f"({disp} dispatches) through oracle/gfq_oracle.c"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            v = d.get("hbm_gbs") or d.get("hbm_GBps")
+            if v:
+                return float(v), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of k_sim from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_k_sim.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+def run_gfq(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2507_08954_b200 import _abi, sweep
+    from paper_2507_08954_b200.engine import Engine
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = sweep.build(args.workload, rank)
+    eng = Engine(local)
+    w.upload(eng)
+    outputs = _abi.WANT_STATS | _abi.WANT_HIST
+    kw = dict(hist_groups=w.groups, hist_rows=w.hist_rows, hist_bins=sweep.HIST_BINS,
+              hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S)
+    sims = w.sims_array()
+    eng.prepare(sims, outputs=outputs, early_exit=True, **kw)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    hist_t = None
+    if world > 1:
+        ptr, n = eng.output_device_ptr(_abi.OUT_HIST)
+        hist_t = torch.as_tensor(_CudaArray(ptr, n, "<i8"), device="cuda")
+
+    def step():
+        eng.launch(stream)
+        if hist_t is not None:
+            dist.all_reduce(hist_t)       # histogram gather over NVLink (NCCL)
+
+    for _ in range(max(args.warmup, 0)):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    eng.synchronize()
+    counters = eng.output(_abi.OUT_COUNTERS).reshape(-1, _abi.NCOUNTERS)
+    disp_per_step = int(counters[:, 2].sum())
+    calls_per_step = int(counters[:, 1].sum())
+    events_per_step = int(counters[:, 0].sum())
+    scans = {"gvt_scans": int(counters[:, 5].sum()), "refresh_scans": int(counters[:, 6].sum()),
+             "candidate_scans": int(counters[:, 7].sum()),
+             "max_dynamic_events": int(counters[:, 4].max())}
+
+    # ---- timed region (device time, CUDA events on the launch stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k)                                  # evict L2 between steps
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    eng.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    t = torch.tensor([tot_ms, float(disp_per_step * args.steps)], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        tm = t[:1].clone(); dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        td = t[1:].clone(); dist.all_reduce(td)
+        max_ms, all_disp = float(tm.item()), float(td.item())
+    else:
+        max_ms, all_disp = tot_ms, float(t[1].item())
+    value = all_disp / (max_ms / 1e3)
+
+    # ---- e2e through the public API with host buffers
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    e2e = e2e_run(eng, w, outputs, kw, e2e_steps, world, dist if world > 1 else None)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    # roofline of the dominant kernel (k_sim): algorithmic bytes per launch
+    n_arr = w.arrivals
+    n_flows = int(sum(w.traces[s.trace].n_flows for s in w.sims))
+    alg_bytes = 12 * n_arr + 32 * n_flows + 76 * len(w.sims)
+    kern_ms = statistics.mean(step_ms)
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    nc = ncu_traffic()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": (nc or {}).get("dram_bytes_per_launch"),
+            "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "note": "k_sim is latency/issue-bound serial event processing; HBM is not binding",
+            "sm_issue_pct_ncu": (nc or {}).get("sm_inst_issued_pct"),
+            "ncu_capture": (nc or {}).get("capture")}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle.oracle as orc
+        orc.build()
+        d, n, dt = cpu_sample(w, args.cpu_seconds, 1)
+        cpu = {"value": d / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{n} random sims of the {args.workload} sweep ({d} dispatches, "
+                         f"{dt:.1f} s) through oracle/gfq_oracle.c, 1 thread"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen_zipf Azure-shaped traces, default profiles; per-rank seed blocks)",
+        "config": dict(w.describe, parallelism=f"sims sharded over {world} GPU(s), "
+                       "warp per simulation", l2="flushed (256 MiB write) before every step",
+                       outputs="per-function stats + latency histograms",
+                       dispatch_calls_per_step=calls_per_step, events_per_step=events_per_step,
+                       dispatches_per_step_per_gpu=disp_per_step, **scans),
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+        "clocks": clk.summary(), "gpu_launches": args.steps,
+        "kernel_ms": {"mean": kern_ms, "min": min(step_ms), "max": max(step_ms)},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of an engine-owned device buffer."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+def e2e_run(eng, w, outputs, kw, steps, world, dist):
+    """Public-API end-to-end: host->device uploads from pinned buffers, one
+    launch, device->host results, every step (wall clock, max over ranks)."""
+    import torch
+    from paper_2507_08954_b200 import _abi
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    arrival = pinned(np.concatenate([t.arrival for t in w.traces]))
+    flow = pinned(np.concatenate([t.flow for t in w.traces]).astype(np.int32))
+    toff = pinned(np.concatenate([[0], np.cumsum([t.n for t in w.traces])]).astype(np.int64))
+    tnf = pinned(np.array([t.n_flows for t in w.traces], dtype=np.int32))
+    cols = [pinned(np.concatenate([getattr(t, c) for t in w.tabs]))
+            for c in ("warm", "cold", "mem", "share", "weight")]
+    hrow = pinned(np.concatenate([t.hist_row for t in w.tabs]).astype(np.int32))
+    tabo = pinned(np.concatenate([[0], np.cumsum([len(t) for t in w.tabs])]).astype(np.int64))
+    h2d = (arrival.nbytes + flow.nbytes + toff.nbytes + tnf.nbytes + sum(c.nbytes for c in cols)
+           + hrow.nbytes + tabo.nbytes + 88 * len(w.dcfgs) + 96 * len(w.sims))
+    n_flows = int(sum(w.traces[s.trace].n_flows for s in w.sims))
+    d2h = 4 * len(w.sims) + 32 * len(w.sims) + 24 * len(w.sims) + 32 * n_flows
+    sims = w.sims_array()
+
+    def one():
+        eng.upload_trace_arrays(arrival, flow, toff, tnf)
+        eng.upload_flowtab_arrays(*cols, hrow, tabo)
+        eng.upload_device_cfgs(w.dcfgs)
+        eng.prepare(sims, outputs=outputs, early_exit=True, **kw)
+        eng.launch()
+        eng.synchronize()
+        n = 0
+        for oid in (_abi.OUT_STATUS, _abi.OUT_COUNTERS, _abi.OUT_SUMMARY, _abi.OUT_FLOW_COUNT,
+                    _abi.OUT_FLOW_MEAN, _abi.OUT_FLOW_VAR, _abi.OUT_FLOW_COLD_PCT):
+            n += eng.output(oid).nbytes
+        c = eng.output(_abi.OUT_COUNTERS).reshape(-1, _abi.NCOUNTERS)
+        return int(c[:, 2].sum()), n
+
+    one()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    disp = 0
+    got = 0
+    for _ in range(steps):
+        d, got = one()
+        disp += d
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([dt, float(disp)], dtype=torch.float64, device="cuda")
+        tm = t[:1].clone(); dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        td = t[1:].clone(); dist.all_reduce(td)
+        dt, disp = float(tm.item()), float(td.item())
+    return {"value": disp / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(got), "d2h_bytes_expected": int(d2h), "steps": steps,
+            "ms_per_step": 1e3 * dt / steps}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gfq(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -42,29 +42,31 @@ namespace gfq {
 // cold_hit_rate (metrics.py:80-84); mean_util (metrics.py:223-226).
 // Lane (f mod 32) owns function f; the completion stream is read 32 records
 // at a time (coalesced) and replayed in order through shuffles.
-__device__ void reduce_stats(WarpSim& w, const Params& p) {
+__device__ __forceinline__ void reduce_stats(WarpSim& w, const Params& p) {
     const int lane = w.lane;
     const int nf = w.nf;
-    const long long nrec = w.n_comp;
-    // reuse the flow slices: vt = latency sum (then mean), lex = its Neumaier
-    // compensation, tau = naive sum, iat/larr = variance sum + compensation,
-    // pt = count, ph = cold count, infl = first-completion rank,
-    // head = rank -> flow, done = variance-pass count
+    const int nrec = w.n_comp;
+    // reuse the flow slices: sum/sumc = latency sum + Neumaier compensation
+    // (then mean), naive = naive sum, var/varc = (x-mean)^2 sum + compensation,
+    // cnt = count, cold = cold count, first = first-completion rank,
+    // order = rank -> flow, vcnt = variance-pass count
+    double *sum = w.vt(), *sumc = w.lex(), *naive = w.tau(), *var = w.iat(), *varc = w.larr();
+    int *cnt = w.pt(), *coldc = w.ph(), *first = w.infl(), *order = w.head(), *vcnt = w.done();
     for (int f = lane; f < nf; f += 32) {
-        w.vt[f] = 0.0; w.lex[f] = 0.0; w.tau[f] = 0.0; w.iat[f] = 0.0; w.larr[f] = 0.0;
-        w.pt[f] = 0; w.ph[f] = 0; w.infl[f] = -1; w.done[f] = 0;
+        sum[f] = 0.0; sumc[f] = 0.0; naive[f] = 0.0; var[f] = 0.0; varc[f] = 0.0;
+        cnt[f] = 0; coldc[f] = 0; first[f] = -1; vcnt[f] = 0;
     }
     __syncwarp();
     const double* lat = p.comp_lat + w.roff;
     const int32_t* meta = p.comp_meta + w.roff;
     int nfirst = 0;
-    long long colds = 0;
+    int colds = 0;
     const bool want_hist = (p.outputs & GFQ_WANT_HIST) && w.sim->group >= 0;
     const double hl0 = want_hist ? log(p.hist_lo) : 0.0;
     const double hscale = want_hist ? (double)p.hist_bins / (log(p.hist_hi) - hl0) : 0.0;
-    const int32_t* hrow = p.hist_row + p.tab_off[w.sim->flowtab];
-    for (long long base = 0; base < nrec; base += 32) {
-        long long k = base + lane;
+    const int32_t* hrow = p.hist_row + w.tb;
+    for (int base = 0; base < nrec; base += 32) {
+        int k = base + lane;
         double x = 0.0; int32_t m = 0;
         if (k < nrec) { x = lat[k]; m = meta[k]; }
         if (want_hist && k < nrec) {
@@ -74,63 +76,62 @@ __device__ void reduce_stats(WarpSim& w, const Params& p) {
             int64_t o = ((int64_t)w.sim->group * p.hist_rows + hrow[fn]) * p.hist_bins + b;
             atomicAdd(&p.hist[o], 1ull);
         }
-        int cnt = (int)min(32ll, nrec - base);
-        for (int j = 0; j < cnt; j++) {
+        int nb = min(32, nrec - base);
+        for (int j = 0; j < nb; j++) {
             double xj = __shfl_sync(FULLMASK, x, j);
             int32_t mj = __shfl_sync(FULLMASK, m, j);
             int fn = mj & 0x7fffffff;
             bool cold = mj < 0;
-            bool first = false;
+            bool isfirst = false;
             if ((fn & 31) == lane) {
-                int c = w.pt[fn];
-                if (c == 0) { first = true; w.vt[fn] = 0.0 + xj; }
+                int c = cnt[fn];
+                if (c == 0) { isfirst = true; sum[fn] = 0.0 + xj; first[fn] = nfirst; }
                 else {
-                    double sf = w.vt[fn];
+                    double sf = sum[fn];
                     double t = sf + xj;
-                    if (fabs(sf) >= fabs(xj)) w.lex[fn] += (sf - t) + xj;
-                    else                      w.lex[fn] += (xj - t) + sf;
-                    w.vt[fn] = t;
+                    if (fabs(sf) >= fabs(xj)) sumc[fn] += (sf - t) + xj;
+                    else                      sumc[fn] += (xj - t) + sf;
+                    sum[fn] = t;
                 }
-                w.tau[fn] = w.tau[fn] + xj;
-                w.pt[fn] = c + 1;
-                if (cold) w.ph[fn] += 1;
-                if (first) w.infl[fn] = nfirst;
+                naive[fn] = naive[fn] + xj;
+                cnt[fn] = c + 1;
+                if (cold) coldc[fn] += 1;
             }
-            if (__ballot_sync(FULLMASK, first)) nfirst++;
+            if (__ballot_sync(FULLMASK, isfirst)) nfirst++;
             colds += cold ? 1 : 0;
         }
     }
     __syncwarp();
     // means, then the second (variance) pass
     for (int f = lane; f < nf; f += 32) {
-        int c = w.pt[f];
-        double sv = w.vt[f], sc = w.lex[f];
+        int c = cnt[f];
+        double sv = sum[f], sc = sumc[f];
         double s = (c == 0) ? 0.0 : ((sc != 0.0 && isfinite(sc)) ? sv + sc : sv);
-        w.vt[f] = c ? s / (double)c : 0.0;                      // mean
-        if (w.infl[f] >= 0) w.head[w.infl[f]] = f;
+        sum[f] = c ? s / (double)c : 0.0;                      // mean
+        if (first[f] >= 0) order[first[f]] = f;
     }
     __syncwarp();
-    for (long long base = 0; base < nrec; base += 32) {
-        long long k = base + lane;
+    for (int base = 0; base < nrec; base += 32) {
+        int k = base + lane;
         double x = 0.0; int32_t m = 0;
         if (k < nrec) { x = lat[k]; m = meta[k]; }
-        int cnt = (int)min(32ll, nrec - base);
-        for (int j = 0; j < cnt; j++) {
+        int nb = min(32, nrec - base);
+        for (int j = 0; j < nb; j++) {
             double xj = __shfl_sync(FULLMASK, x, j);
             int fn = __shfl_sync(FULLMASK, m, j) & 0x7fffffff;
             if ((fn & 31) == lane) {
-                double dx = xj - w.vt[fn];
+                double dx = xj - sum[fn];
                 double v = dx * dx;                      // (x - mean) ** 2
-                int c = w.done[fn];
-                if (c == 0) { w.iat[fn] = 0.0 + v; }
+                int c = vcnt[fn];
+                if (c == 0) { var[fn] = 0.0 + v; }
                 else {
-                    double sf = w.iat[fn];
+                    double sf = var[fn];
                     double t = sf + v;
-                    if (fabs(sf) >= fabs(v)) w.larr[fn] += (sf - t) + v;
-                    else                     w.larr[fn] += (v - t) + sf;
-                    w.iat[fn] = t;
+                    if (fabs(sf) >= fabs(v)) varc[fn] += (sf - t) + v;
+                    else                     varc[fn] += (v - t) + sf;
+                    var[fn] = t;
                 }
-                w.done[fn] = c + 1;
+                vcnt[fn] = c + 1;
             }
         }
     }
@@ -138,89 +139,78 @@ __device__ void reduce_stats(WarpSim& w, const Params& p) {
     const int64_t fo = p.sim_foff[w.sid];
     if (p.outputs & GFQ_WANT_STATS) {
         for (int f = lane; f < nf; f += 32) {
-            int c = w.pt[f];
-            double vf = w.iat[f], vc = w.larr[f];
+            int c = cnt[f];
+            double vf = var[f], vc = varc[f];
             double vs = (c == 0) ? 0.0 : ((vc != 0.0 && isfinite(vc)) ? vf + vc : vf);
             p.f_count[fo + f] = c;
-            p.f_mean[fo + f] = w.vt[f];
+            p.f_mean[fo + f] = sum[f];
             p.f_var[fo + f] = c > 1 ? vs / (double)(c - 1) : 0.0;
-            p.f_cold[fo + f] = c ? 100.0 * (double)w.ph[f] / (double)c : 0.0;
+            p.f_cold[fo + f] = c ? 100.0 * (double)coldc[f] / (double)c : 0.0;
         }
     }
     // weighted_avg_latency: builtin sum over functions in first-completion order
     PySum num; ps_init(num);
     for (int r = 0; r < nfirst; r++) {
-        int f = w.head[r];
-        double nn = (double)w.pt[f];
-        ps_add(num, nn * (w.tau[f] / nn));
+        int f = order[r];
+        double nn = (double)cnt[f];
+        ps_add(num, nn * (naive[f] / nn));
     }
     if (lane == 0) {
-        double* sm = p.summary + (int64_t)w.sid * 3;
-        sm[0] = nrec > 0 ? ps_val(num) / (double)nrec : 0.0;
-        sm[1] = nrec > 0 ? 100.0 * ((double)colds / (double)nrec) : 0.0;
-        sm[2] = w.n_util ? ps_val(w.util_sum) / (double)w.n_util : 0.0;
+        double* smy = p.summary + (int64_t)w.sid * 3;
+        smy[0] = nrec > 0 ? ps_val(num) / (double)nrec : 0.0;
+        smy[1] = nrec > 0 ? 100.0 * ((double)colds / (double)nrec) : 0.0;
+        smy[2] = w.n_util ? ps_val(w.util_sum) / (double)w.n_util : 0.0;
     }
 }
 
-__device__ void run_one(const Params& p, unsigned char* base, int lane, int sid) {
-    const Layout& L = p.L;
-    WarpSim w;
-    w.P = &p; w.L = &L; w.lane = lane; w.sid = sid;
-    w.vt = (double*)(base + L.o_vt); w.lex = (double*)(base + L.o_lex);
-    w.tau = (double*)(base + L.o_tau); w.iat = (double*)(base + L.o_iat);
-    w.larr = (double*)(base + L.o_larr);
-    w.pt = (int*)(base + L.o_pt); w.ph = (int*)(base + L.o_ph); w.infl = (int*)(base + L.o_infl);
-    w.head = (int*)(base + L.o_head); w.done = (int*)(base + L.o_done);
-    w.fst = (uint8_t*)(base + L.o_fst);
-    w.ev_t = (double*)(base + L.o_ev_t); w.ev_seq = (uint32_t*)(base + L.o_ev_seq);
-    w.ev_meta = (uint32_t*)(base + L.o_ev_meta);
-    w.dvi = (int*)(base + L.o_dvi); w.dvd = (double*)(base + L.o_dvd);
-    w.smp_t = (double*)(base + L.o_smp_t); w.smp_u = (double*)(base + L.o_smp_u);
-    w.run_i = (int*)(base + L.o_run_i); w.run_d = (double*)(base + L.o_run_d);
-    w.pool_m = (uint32_t*)(base + L.o_pool_m); w.pool_t = (double*)(base + L.o_pool_t);
-    w.cnt = (uint16_t*)(base + L.o_cnt);
-
+__device__ __forceinline__ void run_one(const Params& p, unsigned char* base, int lane, int sid) {
+    WarpSim w(p, base, lane, sid);
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
     const int t = sim->trace;
-    const int64_t toff = p.trace_off[t];
-    w.n = (int)(p.trace_off[t + 1] - toff);
+    w.toff = p.trace_off[t];
+    w.n = (int)(p.trace_off[t + 1] - w.toff);
     w.nf = p.trace_nf[t];
-    w.arr = p.arrival + toff; w.flw = p.flow + toff;
-    w.foff = p.foff + p.foff_off[t]; w.fpos = p.fpos + toff;
-    const int64_t tb = p.tab_off[sim->flowtab];
-    w.warm = p.warm + tb; w.cold = p.cold + tb; w.mem = p.mem + tb;
-    w.share = p.share + tb; w.weight = p.weight + tb;
+    w.foff = p.foff + p.foff_off[t];
+    w.tb = p.tab_off[sim->flowtab];
+    w.roff = p.sim_roff[sid];
     w.policy = sim->policy;
     w.scripted = sim->device_model == GFQ_DEVMODEL_SCRIPTED;
     w.mqfq = sim->policy == GFQ_POLICY_MQFQ;
     w.fcfs = sim->policy == GFQ_POLICY_FCFS || sim->policy == GFQ_POLICY_FCFS_NAIVE;
-    w.dc = p.dcfg + (w.scripted ? 0 : sim->device_cfg);
     w.ndev = w.scripted ? 1 : sim->n_devices;
-    w.execs = p.execs;
     w.T = sim->t_overrun; w.alpha = sim->alpha; w.dttl = sim->default_ttl_s;
-    w.roff = p.sim_roff[sid];
-    w.foffs = p.sim_foff[sid];
 
     // ---- reset the workspace
-    for (int f = lane; f < w.nf; f += 32) {
-        w.vt[f] = 0.0; w.lex[f] = 0.0; w.tau[f] = 0.0; w.iat[f] = 0.0; w.larr[f] = 0.0;
-        w.pt[f] = 0; w.ph[f] = 0; w.infl[f] = 0; w.head[f] = -1; w.done[f] = 0; w.fst[f] = 0;
+    {
+        double *vt = w.vt(), *lex = w.lex(), *tau = w.tau(), *iat = w.iat(), *larr = w.larr();
+        int *pt = w.pt(), *ph = w.ph(), *infl = w.infl(), *head = w.head(), *done = w.done(), *pend = w.pend();
+        uint8_t* fst = w.fst();
+        for (int f = lane; f < w.nf; f += 32) {
+            vt[f] = 0.0; lex[f] = 0.0; tau[f] = 0.0; iat[f] = 0.0; larr[f] = 0.0;
+            pt[f] = 0; ph[f] = 0; infl[f] = 0; head[f] = -1; done[f] = 0; pend[f] = 0; fst[f] = 0;
+        }
+        uint16_t* cnt = (uint16_t*)(base + p.L.o_cnt);
+        for (int i = lane; i < 3 * w.ndev * p.L.F; i += 32) cnt[i] = 0;
+        if (lane < w.ndev) {
+            int d = lane;
+            int* dvi = (int*)(base + p.L.o_dvi);
+            double* dvd = (double*)(base + p.L.o_dvd);
+            int dmax = w.scripted ? sim->scripted_d : p.dcfg[sim->device_cfg + d].d_max;
+            dvi[d * 8 + DV_OUT] = 0;
+            dvi[d * 8 + DV_EFFD] = dmax;
+            dvi[d * 8 + DV_NP] = 0; dvi[d * 8 + DV_NRUN] = 0;
+            dvi[d * 8 + DV_SHEAD] = 0; dvi[d * 8 + DV_SN] = 0;
+            dvi[d * 8 + DV_HROK] = w.scripted ? 1
+                : !(0.0 + 1.0 / (double)dmax > p.dcfg[sim->device_cfg + d].util_threshold);
+            dvd[d * 2] = 0.0; dvd[d * 2 + 1] = 0.0;
+        }
+        __syncwarp();
     }
-    for (int i = lane; i < 2 * w.ndev * L.F; i += 32) w.cnt[i] = 0;
-    if (lane < w.ndev) {
-        int d = lane;
-        w.dvi[d * 8 + DV_OUT] = 0;
-        w.dvi[d * 8 + DV_EFFD] = w.scripted ? sim->scripted_d : w.dc[d].d_max;
-        w.dvi[d * 8 + DV_NP] = 0; w.dvi[d * 8 + DV_NRUN] = 0;
-        w.dvi[d * 8 + DV_SHEAD] = 0; w.dvi[d * 8 + DV_SN] = 0;
-        w.dvd[d * 2] = 0.0; w.dvd[d * 2 + 1] = 0.0;
-    }
-    __syncwarp();
     w.period = 0.0;
     if (!w.scripted) {                                   // engine.py:80-81
-        w.period = w.dc[0].monitor_period_s;
-        for (int d = 1; d < w.ndev; d++) w.period = pymin(w.period, w.dc[d].monitor_period_s);
+        w.period = w.dc(0).monitor_period_s;
+        for (int d = 1; d < w.ndev; d++) w.period = pymin(w.period, w.dc(d).monitor_period_s);
     }
     w.now = 0.0; w.gvt = 0.0;
     w.seq = (uint32_t)w.n;
@@ -231,7 +221,11 @@ __device__ void run_one(const Params& p, unsigned char* base, int lane, int sid)
     w.fcfs_head = 0; w.fcfs_infl = 0; w.draining = -1;
     w.s_att = 0; w.s_out = 0; w.s_exec = 0;
     w.status = 0; w.any_newly = false;
-    w.n_events = w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
+    w.gmin_ok = false; w.gmin = ~0ull;
+    w.idle_lb = __longlong_as_double(0x7ff0000000000000ll);
+    w.n_events = 0;
+    w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
+    w.max_ev = w.n_gscan = w.n_rscan = w.n_cscan = 0;
     ps_init(w.util_sum);
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
@@ -243,8 +237,9 @@ __device__ void run_one(const Params& p, unsigned char* base, int lane, int sid)
     if (!w.status) reduce_stats(w, p);
     if (lane == 0) {
         p.status[sid] = w.status;
-        int64_t* c = p.counters + (int64_t)sid * 4;
-        c[0] = w.n_events; c[1] = w.n_calls; c[2] = w.n_disp; c[3] = w.n_util;
+        int64_t* c = p.counters + (int64_t)sid * GFQ_NCOUNTERS;
+        c[C_EVENTS] = w.n_events; c[C_CALLS] = w.n_calls; c[C_DISP] = w.n_disp; c[C_UTIL] = w.n_util;
+        c[C_MAXEV] = w.max_ev; c[C_GSCAN] = w.n_gscan; c[C_RSCAN] = w.n_rscan; c[C_CSCAN] = w.n_cscan;
         p.final_time[sid] = w.now;
         if (p.outputs & GFQ_WANT_AUDIT) p.backlog_count[sid] = w.n_backlog;
         if (p.outputs & GFQ_WANT_EVENTS) p.event_count[sid] = w.n_evlog;
@@ -646,7 +641,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))))
         return rc;
     for (int id = 0; id < GFQ_OUT_COUNT_; id++) h->out_n[id] = 0;
-    if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, 4ll * n_sims)) ||
+    if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, (int64_t)GFQ_NCOUNTERS * n_sims)) ||
         (rc = alloc_out(h, GFQ_OUT_FINAL_TIME, n_sims)) || (rc = alloc_out(h, GFQ_OUT_SUMMARY, 3ll * n_sims)))
         return rc;
     if (c.outputs & GFQ_WANT_STATS)

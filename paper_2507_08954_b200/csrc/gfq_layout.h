@@ -17,7 +17,7 @@ namespace gfq {
 enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
 
 // per-device int fields
-enum { DV_OUT = 0, DV_EFFD, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_NI };
+enum { DV_OUT = 0, DV_EFFD, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_HROK, DV_NI };
 
 // event kinds (engine.py:20-23)
 enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };
@@ -31,14 +31,14 @@ struct Layout {
     int32_t S;      // utilization-sample ring slots per device
     // byte offsets inside one warp's slice (all 8-byte aligned)
     int32_t o_vt, o_lex, o_tau, o_iat, o_larr;          // f64[F]
-    int32_t o_pt, o_ph, o_infl, o_head, o_done;          // i32[F]
+    int32_t o_pt, o_ph, o_infl, o_head, o_done, o_pend;  // i32[F]
     int32_t o_fst;                                       // u8[F]
     int32_t o_ev_t, o_ev_seq, o_ev_meta;                 // f64[E], u32[E], u32[E]
     int32_t o_dvi, o_dvd;                                // i32[ND][8], f64[ND][2]
     int32_t o_smp_t, o_smp_u;                            // f64[ND][S]
     int32_t o_run_i, o_run_d;                            // i32[ND][R][4], f64[ND][R][2]
     int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
-    int32_t o_cnt;                                       // u16[ND][2][F]
+    int32_t o_cnt;                                       // u16[ND][3][F]: gpu-warm, host-warm, running
     int32_t bytes;                                       // slice size
 };
 
@@ -68,7 +68,7 @@ struct Params {
     int32_t early_exit;
     // outputs
     int32_t* status;
-    int64_t* counters;             // [sims][4]
+    int64_t* counters;             // [sims][GFQ_NCOUNTERS]
     double* final_time;
     double* summary;               // [sims][3]
     int64_t* f_count; double* f_mean; double* f_var; double* f_cold;
@@ -93,14 +93,14 @@ inline void layout_finish(Layout& L) {
     L.o_vt = take(8 * F); L.o_lex = take(8 * F); L.o_tau = take(8 * F);
     L.o_iat = take(8 * F); L.o_larr = take(8 * F);
     L.o_pt = take(4 * F); L.o_ph = take(4 * F); L.o_infl = take(4 * F);
-    L.o_head = take(4 * F); L.o_done = take(4 * F);
+    L.o_head = take(4 * F); L.o_done = take(4 * F); L.o_pend = take(4 * F);
     L.o_fst = take(F);
     L.o_ev_t = take(8 * E); L.o_ev_seq = take(4 * E); L.o_ev_meta = take(4 * E);
     L.o_dvi = take(4 * 8 * ND); L.o_dvd = take(8 * 2 * ND);
     L.o_smp_t = take(8 * ND * S); L.o_smp_u = take(8 * ND * S);
     L.o_run_i = take(4 * 4 * ND * R); L.o_run_d = take(8 * 2 * ND * R);
     L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);
-    L.o_cnt = take(2 * 2 * ND * F);
+    L.o_cnt = take(2 * 3 * ND * F);
     L.bytes = o;
 }
 

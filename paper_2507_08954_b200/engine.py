@@ -113,6 +113,18 @@ class Engine:
         check(self._L.gfq_upload_traces(self._h, _ptr(arrival, C.c_double), _ptr(flow, C.c_int32),
                                         _ptr(off, C.c_int64), _ptr(nf, C.c_int32), len(traces)))
 
+    def upload_trace_arrays(self, arrival, flow, off, n_flows) -> None:
+        """Pre-packed CSR arrays (e.g. pinned host buffers), no host copy."""
+        check(self._L.gfq_upload_traces(self._h, _ptr(arrival, C.c_double), _ptr(flow, C.c_int32),
+                                        _ptr(off, C.c_int64), _ptr(n_flows, C.c_int32),
+                                        int(n_flows.shape[0])))
+
+    def upload_flowtab_arrays(self, warm, cold, mem, share, weight, hist_row, off) -> None:
+        check(self._L.gfq_upload_flowtabs(
+            self._h, _ptr(warm, C.c_double), _ptr(cold, C.c_double), _ptr(mem, C.c_double),
+            _ptr(share, C.c_double), _ptr(weight, C.c_double), _ptr(hist_row, C.c_int32),
+            _ptr(off, C.c_int64), int(off.shape[0]) - 1))
+
     def upload_flowtabs(self, tabs) -> None:
         cols = {}
         for name in ("warm", "cold", "mem", "share", "weight"):
@@ -226,7 +238,7 @@ class BatchResult:
 
     @property
     def counters(self):
-        return self.get(_abi.OUT_COUNTERS).reshape(-1, 4)
+        return self.get(_abi.OUT_COUNTERS).reshape(-1, _abi.NCOUNTERS)
 
     @property
     def summary(self):

@@ -1,0 +1,124 @@
+"""Batched sweeps: the BASELINE.json configurations as engine batches.
+
+The reference runs sweeps serially, one ``run_experiment`` per grid point
+(cli.py:131-163 ``cmd_sweep``; cli.py:67-116 ``cmd_compare``).  Here a sweep
+is one upload of its distinct traces and flow tables plus one
+``gfq_sim`` parameter block per grid point, run in a single kernel launch.
+
+* ``c3`` — BASELINE C3 (configs[2]): F=100 default profiles, Zipf s=1.5,
+  2.382870 rps (rho = 1), 600 s; T in {0,1,2,5,10,20,50,100} x alpha in
+  {0,.5,1,1.5,2,3,4,8} x D in {1,2,3,4} x 16 seeds = 4096 MQFQ-Sticky sims.
+* ``c2`` — BASELINE C2 (configs[1]): F=200, Zipf 1.5, the paper's Table 3
+  request rates x seeds x {mqfq, fcfs, batch}, 600 s.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .device import DeviceConfig
+from .engine import sim_params
+from .mqfq import SchedulerConfig
+from .pack import FlowTable, PackedTrace, flow_table, pack_trace
+from .workload import default_profiles, gen_zipf
+
+C3_T = [0.0, 1.0, 2.0, 5.0, 10.0, 20.0, 50.0, 100.0]
+C3_ALPHA = [0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 8.0]
+C3_D = [1, 2, 3, 4]
+C3_RATE = 2.382870
+TABLE3_RPS = [1.12, 1.69, 1.94, 4.26, 2.69, 2.57, 2.55, 1.79, 1.12]
+
+
+@dataclass
+class Workload:
+    name: str
+    traces: list[PackedTrace]
+    tabs: list[FlowTable]
+    dcfgs: list
+    sims: list
+    groups: int
+    hist_rows: int
+    describe: dict
+
+    @property
+    def arrivals(self) -> int:
+        return int(sum(self.traces[s.trace].n for s in self.sims))
+
+    def upload(self, eng) -> None:
+        eng.upload_traces(self.traces)
+        eng.upload_flowtabs(self.tabs)
+        eng.upload_device_cfgs(self.dcfgs)
+
+    def sims_array(self):
+        arr = (_abi.Sim * len(self.sims))(*self.sims)
+        return arr
+
+
+def _traces(n_fn, s, rates_seeds, duration):
+    profiles = default_profiles(n_fn)
+    order = {nm: i for i, nm in enumerate(profiles)}
+    traces, tabs = [], []
+    for rate, seed in rates_seeds:
+        tr = gen_zipf(n_fn, s, rate, duration, seed)
+        pt = pack_trace(tr.entries, profiles)
+        traces.append(pt)
+        # histogram row = the function's identity (profile index), not its
+        # per-trace rank, so rows line up across traces and GPUs
+        tabs.append(flow_table(pt.names, profiles, None, [order[nm] for nm in pt.names]))
+    return traces, tabs
+
+
+def c3(seed_base: int = 1, n_seeds: int = 16, duration: float = 600.0) -> Workload:
+    seeds = list(range(seed_base, seed_base + n_seeds))
+    traces, tabs = _traces(100, 1.5, [(C3_RATE, s) for s in seeds], duration)
+    dcfgs = [DeviceConfig(d_max=d) for d in C3_D]
+    sims = []
+    for ti, t in enumerate(C3_T):
+        for ai, a in enumerate(C3_ALPHA):
+            cfg = SchedulerConfig(t_overrun=t, alpha=a)
+            for di, d in enumerate(C3_D):
+                for si in range(n_seeds):
+                    sims.append(sim_params("mqfq", cfg, 1, trace=si, flowtab=si, device_cfg=di,
+                                           group=ti * len(C3_ALPHA) + ai))
+    return Workload("c3", traces, tabs, dcfgs, sims, groups=len(C3_T) * len(C3_ALPHA),
+                    hist_rows=100,
+                    describe={"workload": "C3 MQFQ-Sticky sweep: T x alpha x D x seeds",
+                              "functions": 100, "zipf_s": 1.5, "rate_rps": C3_RATE,
+                              "duration_s": duration, "seeds": [seeds[0], seeds[-1]],
+                              "grid": "8 T x 8 alpha x 4 D", "sims": len(sims)})
+
+
+def c2(seed_base: int = 1, n_seeds: int = 456, duration: float = 600.0,
+       policies=("mqfq", "fcfs", "batch")) -> Workload:
+    rs = [(r, s) for s in range(seed_base, seed_base + n_seeds) for r in TABLE3_RPS]
+    traces, tabs = _traces(200, 1.5, rs, duration)
+    dcfgs = [DeviceConfig()]
+    sims = []
+    cfg = SchedulerConfig()
+    for ti in range(len(traces)):
+        for pi, pol in enumerate(policies):
+            sims.append(sim_params(pol, cfg, 1, trace=ti, flowtab=ti, device_cfg=0, group=pi))
+    return Workload("c2", traces, tabs, dcfgs, sims, groups=len(policies), hist_rows=200,
+                    describe={"workload": "C2 Azure-shaped: Table-3 rates x seeds x policies",
+                              "functions": 200, "zipf_s": 1.5, "duration_s": duration,
+                              "traces": len(traces), "policies": list(policies),
+                              "sims": len(sims)})
+
+
+def build(name: str, rank: int = 0, **kw) -> Workload:
+    """Weak-scaling shard for `rank`: a disjoint block of seeds per GPU."""
+    if name == "c3":
+        n = kw.get("n_seeds", 16)
+        return c3(seed_base=1 + rank * n, n_seeds=n)
+    if name == "c2":
+        n = kw.get("n_seeds", 456)
+        return c2(seed_base=1 + rank * n, n_seeds=n)
+    raise ValueError(f"unknown workload {name}")
+
+
+HIST_BINS = 64
+HIST_LO_S = 1e-2
+HIST_HI_S = 1e5
