@@ -15,7 +15,7 @@ import threading
 from . import _abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgfq.so")
+LIB_PATH = os.environ.get("GFQ_LIB") or os.path.join(HERE, "libgfq.so")
 
 _lib = None
 _lock = threading.Lock()

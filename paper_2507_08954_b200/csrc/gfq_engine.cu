@@ -42,29 +42,31 @@ namespace gfq {
 // cold_hit_rate (metrics.py:80-84); mean_util (metrics.py:223-226).
 // Lane (f mod 32) owns function f; the completion stream is read 32 records
 // at a time (coalesced) and replayed in order through shuffles.
-__device__ __forceinline__ void reduce_stats(WarpSim& w, const Params& p) {
-    const int lane = w.lane;
-    const int nf = w.nf;
-    const int nrec = w.n_comp;
-    // reuse the flow slices: sum/sumc = latency sum + Neumaier compensation
+__device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base, int lane, int sid) {
+    const gfq_sim* sim = p.sims + sid;
+    const int nf = p.trace_nf[sim->trace];
+    const int nrec = (int)p.counters[(int64_t)sid * GFQ_NCOUNTERS + C_DISP];
+    const int64_t roff = p.sim_roff[sid], tb = p.tab_off[sim->flowtab];
+    const int F = p.L.F;
+    // per-warp scratch: sum/sumc = latency sum + Neumaier compensation
     // (then mean), naive = naive sum, var/varc = (x-mean)^2 sum + compensation,
     // cnt = count, cold = cold count, first = first-completion rank,
     // order = rank -> flow, vcnt = variance-pass count
-    double *sum = w.vt(), *sumc = w.lex(), *naive = w.tau(), *var = w.iat(), *varc = w.larr();
-    int *cnt = w.pt(), *coldc = w.ph(), *first = w.infl(), *order = w.head(), *vcnt = w.done();
+    double *sum = (double*)base, *sumc = sum + F, *naive = sum + 2 * F, *var = sum + 3 * F, *varc = sum + 4 * F;
+    int *cnt = (int*)(sum + 5 * F), *coldc = cnt + F, *first = cnt + 2 * F, *order = cnt + 3 * F, *vcnt = cnt + 4 * F;
     for (int f = lane; f < nf; f += 32) {
         sum[f] = 0.0; sumc[f] = 0.0; naive[f] = 0.0; var[f] = 0.0; varc[f] = 0.0;
         cnt[f] = 0; coldc[f] = 0; first[f] = -1; vcnt[f] = 0;
     }
     __syncwarp();
-    const double* lat = p.comp_lat + w.roff;
-    const int32_t* meta = p.comp_meta + w.roff;
+    const double* lat = p.comp_lat + roff;
+    const int32_t* meta = p.comp_meta + roff;
     int nfirst = 0;
     int colds = 0;
-    const bool want_hist = (p.outputs & GFQ_WANT_HIST) && w.sim->group >= 0;
+    const bool want_hist = (p.outputs & GFQ_WANT_HIST) && sim->group >= 0;
     const double hl0 = want_hist ? log(p.hist_lo) : 0.0;
     const double hscale = want_hist ? (double)p.hist_bins / (log(p.hist_hi) - hl0) : 0.0;
-    const int32_t* hrow = p.hist_row + w.tb;
+    const int32_t* hrow = p.hist_row + tb;
     for (int base = 0; base < nrec; base += 32) {
         int k = base + lane;
         double x = 0.0; int32_t m = 0;
@@ -73,7 +75,7 @@ __device__ __forceinline__ void reduce_stats(WarpSim& w, const Params& p) {
             int fn = m & 0x7fffffff;
             int b = x > 0.0 ? (int)floor((log(x) - hl0) * hscale) : 0;
             b = max(0, min(p.hist_bins - 1, b));
-            int64_t o = ((int64_t)w.sim->group * p.hist_rows + hrow[fn]) * p.hist_bins + b;
+            int64_t o = ((int64_t)sim->group * p.hist_rows + hrow[fn]) * p.hist_bins + b;
             atomicAdd(&p.hist[o], 1ull);
         }
         int nb = min(32, nrec - base);
@@ -136,7 +138,7 @@ __device__ __forceinline__ void reduce_stats(WarpSim& w, const Params& p) {
         }
     }
     __syncwarp();
-    const int64_t fo = p.sim_foff[w.sid];
+    const int64_t fo = p.sim_foff[sid];
     if (p.outputs & GFQ_WANT_STATS) {
         for (int f = lane; f < nf; f += 32) {
             int c = cnt[f];
@@ -156,15 +158,16 @@ __device__ __forceinline__ void reduce_stats(WarpSim& w, const Params& p) {
         ps_add(num, nn * (naive[f] / nn));
     }
     if (lane == 0) {
-        double* smy = p.summary + (int64_t)w.sid * 3;
+        double* smy = p.summary + (int64_t)sid * 3;
         smy[0] = nrec > 0 ? ps_val(num) / (double)nrec : 0.0;
         smy[1] = nrec > 0 ? 100.0 * ((double)colds / (double)nrec) : 0.0;
-        smy[2] = w.n_util ? ps_val(w.util_sum) / (double)w.n_util : 0.0;
     }
 }
 
+
+template <bool G>
 __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, int lane, int sid) {
-    WarpSim w(p, base, lane, sid);
+    WarpSim<G> w(p, base, lane, sid);
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
     const int t = sim->trace;
@@ -175,11 +178,13 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
     w.tb = p.tab_off[sim->flowtab];
     w.roff = p.sim_roff[sid];
     w.policy = sim->policy;
-    w.scripted = sim->device_model == GFQ_DEVMODEL_SCRIPTED;
-    w.mqfq = sim->policy == GFQ_POLICY_MQFQ;
-    w.fcfs = sim->policy == GFQ_POLICY_FCFS || sim->policy == GFQ_POLICY_FCFS_NAIVE;
-    w.ndev = w.scripted ? 1 : sim->n_devices;
+    w.scripted_ = sim->device_model == GFQ_DEVMODEL_SCRIPTED;
+    w.mqfq_ = sim->policy == GFQ_POLICY_MQFQ;
+    w.fcfs_ = sim->policy == GFQ_POLICY_FCFS || sim->policy == GFQ_POLICY_FCFS_NAIVE;
+    const bool scripted = G && w.scripted_;
+    w.ndev = scripted ? 1 : sim->n_devices;
     w.T = sim->t_overrun; w.alpha = sim->alpha; w.dttl = sim->default_ttl_s;
+    w.tau_inc = sim->tau_includes_overheads != 0;
 
     // ---- reset the workspace
     {
@@ -194,23 +199,31 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
         for (int i = lane; i < 3 * w.ndev * p.L.F; i += 32) cnt[i] = 0;
         if (lane < w.ndev) {
             int d = lane;
-            int* dvi = (int*)(base + p.L.o_dvi);
-            double* dvd = (double*)(base + p.L.o_dvd);
-            int dmax = w.scripted ? sim->scripted_d : p.dcfg[sim->device_cfg + d].d_max;
-            dvi[d * 8 + DV_OUT] = 0;
-            dvi[d * 8 + DV_EFFD] = dmax;
-            dvi[d * 8 + DV_NP] = 0; dvi[d * 8 + DV_NRUN] = 0;
-            dvi[d * 8 + DV_SHEAD] = 0; dvi[d * 8 + DV_SN] = 0;
-            dvi[d * 8 + DV_HROK] = w.scripted ? 1
-                : !(0.0 + 1.0 / (double)dmax > p.dcfg[sim->device_cfg + d].util_threshold);
-            dvd[d * 2] = 0.0; dvd[d * 2 + 1] = 0.0;
+            int* dvi = (int*)(base + p.L.o_dvi) + d * DV_NI;
+            double* dvd = (double*)(base + p.L.o_dvd) + d * DD_ND;
+            for (int k = 0; k < DV_NI; k++) dvi[k] = 0;
+            for (int k = 0; k < DD_ND; k++) dvd[k] = 0.0;
+            if (scripted) {
+                dvi[DV_DMAX] = sim->scripted_d; dvi[DV_EFFD] = sim->scripted_d; dvi[DV_HROK] = 1;
+            } else {
+                const gfq_device_cfg& c = p.dcfg[sim->device_cfg + d];
+                dvi[DV_DMAX] = c.d_max; dvi[DV_EFFD] = c.d_max;
+                dvi[DV_POOLMAX] = c.pool_max_containers; dvi[DV_POOLON] = c.pool_enabled != 0;
+                dvi[DV_DYN] = c.dynamic_d != 0;
+                dvd[DD_MEMCAP] = c.mem_capacity_mb; dvd[DD_THR] = c.util_threshold;
+                dvd[DD_PCIE] = c.pcie_mb_per_s; dvd[DD_BETA] = c.interference_beta;
+                dvd[DD_WINDOW] = c.util_window_s; dvd[DD_OVERLAP] = c.prefetch_overlap_s;
+                dvd[DD_INVDMAX] = 1.0 / (double)c.d_max;
+                dvi[DV_HROK] = !(0.0 + dvd[DD_INVDMAX] > c.util_threshold);
+                dvi[DV_CACHE_N] = -1;
+            }
         }
         __syncwarp();
     }
     w.period = 0.0;
-    if (!w.scripted) {                                   // engine.py:80-81
-        w.period = w.dc(0).monitor_period_s;
-        for (int d = 1; d < w.ndev; d++) w.period = pymin(w.period, w.dc(d).monitor_period_s);
+    if (!scripted) {                                   // engine.py:80-81
+        w.period = p.dcfg[sim->device_cfg].monitor_period_s;
+        for (int d = 1; d < w.ndev; d++) w.period = pymin(w.period, p.dcfg[sim->device_cfg + d].monitor_period_s);
     }
     w.now = 0.0; w.gvt = 0.0;
     w.seq = (uint32_t)w.n;
@@ -230,13 +243,13 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
     // tick (only when the trace is non-empty) seq n
-    if (w.n > 0 && !w.scripted) w.push(w.period, EV_TICK, 0);
+    if (w.n > 0 && !scripted) w.push(w.period, EV_TICK, 0);
 
     w.run();
 
-    if (!w.status) reduce_stats(w, p);
     if (lane == 0) {
         p.status[sid] = w.status;
+        p.summary[(int64_t)sid * 3 + 2] = w.n_util ? ps_val(w.util_sum) / (double)w.n_util : 0.0;
         int64_t* c = p.counters + (int64_t)sid * GFQ_NCOUNTERS;
         c[C_EVENTS] = w.n_events; c[C_CALLS] = w.n_calls; c[C_DISP] = w.n_disp; c[C_UTIL] = w.n_util;
         c[C_MAXEV] = w.max_ev; c[C_GSCAN] = w.n_gscan; c[C_RSCAN] = w.n_rscan; c[C_CSCAN] = w.n_cscan;
@@ -252,7 +265,11 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(256) k_sim(const __grid_constant__ Params p) {
+#ifndef GFQ_MINB
+#define GFQ_MINB 4
+#endif
+template <bool G>
+__global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* base = smem + (size_t)warp * p.L.bytes;
@@ -261,8 +278,19 @@ __global__ void __launch_bounds__(256) k_sim(const __grid_constant__ Params p) {
         if (lane == 0) idx = atomicAdd(p.work, 1);
         idx = __shfl_sync(FULLMASK, idx, 0);
         if (idx >= p.n_sims) break;
-        run_one(p, base, lane, p.order[idx]);
+        run_one<G>(p, base, lane, p.order[idx]);
     }
+}
+
+// Result reducer: one warp per finished simulation, over its completion
+// stream (comp_lat / comp_meta, written in completion order by k_sim).
+__global__ void __launch_bounds__(128) k_reduce(const __grid_constant__ Params p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sid = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (sid >= p.n_sims) return;
+    if (p.status[sid] != GFQ_SIM_OK) return;
+    reduce_one(p, smem + (size_t)warp * 60 * p.L.F, lane, sid);
 }
 
 // Trace loader: one warp per trace.  Counting sort of trace positions by
@@ -370,7 +398,8 @@ struct gfq_handle {
     int32_t n_sims = 0;
     gfq_launch_cfg cfg{};
     Layout L{};
-    int wpb = 0, blocks = 0;
+    int wpb = 0, blocks = 0, rwpb = 4;
+    bool generic = true;
     bool prepared = false;
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
@@ -624,15 +653,30 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     if ((size_t)L.bytes > h->smem_optin)
         return set_err(GFQ_EINVAL, "gfq_prepare: per-simulation workspace (" + std::to_string(L.bytes) +
                                        " B) exceeds shared memory; reduce flows/pool/event capacity");
-    int wpb = c.warps_per_block > 0 ? c.warps_per_block : 4;
+    // the MQFQ-Sticky / DeviceSet build unless a sim or an output needs the
+    // generic one (other policies, scripted devices, audit / event logs)
+    bool generic = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
+    for (int i = 0; i < n_sims && !generic; i++)
+        generic = sims[i].policy != GFQ_POLICY_MQFQ || sims[i].device_model != GFQ_DEVMODEL_DEVICESET;
+    const void* kfn = generic ? (const void*)k_sim<true> : (const void*)k_sim<false>;
+    int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, 4) : 4;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
     size_t smem = (size_t)wpb * L.bytes;
-    CK(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // all of the unified L1/shared array to shared memory: occupancy is bounded
+    // by per-warp simulation state; the kernel's global traffic is tiny
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            (int)cudaSharedmemCarveoutMaxShared));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim, wpb * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, wpb * 32, smem));
     if (per_sm < 1) return set_err(GFQ_EINVAL, "gfq_prepare: kernel does not fit on an SM");
     int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
     blocks = std::max(1, std::min(blocks, (n_sims + wpb - 1) / wpb));
+    int rwpb = 4;
+    while (rwpb > 1 && (size_t)rwpb * 60 * L.F > h->smem_optin) rwpb--;
+    if ((size_t)rwpb * 60 * L.F > h->smem_optin)
+        return set_err(GFQ_EINVAL, "gfq_prepare: too many flows per simulation for the reducer");
+    CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(rwpb * 60 * L.F)));
 
     int rc;
     if ((rc = h->sims.ensure(sizeof(gfq_sim) * std::max(n_sims, 1))) || (rc = h->order.ensure(4 * std::max(n_sims, 1))) ||
@@ -695,6 +739,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->L = L;
     h->wpb = wpb;
     h->blocks = blocks;
+    h->rwpb = rwpb;
+    h->generic = generic;
     h->prepared = true;
     h->launched = false;
     return GFQ_OK;
@@ -765,10 +811,16 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(h->ev[0], st));
     if (h->n_sims > 0) {
         size_t smem = (size_t)h->wpb * h->L.bytes;
-        k_sim<<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        if (h->generic) k_sim<true><<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        else k_sim<false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[1], st));
+    if (h->n_sims > 0) {
+        int rb = (h->n_sims + h->rwpb - 1) / h->rwpb;
+        k_reduce<<<rb, h->rwpb * 32, (size_t)h->rwpb * 60 * h->L.F, st>>>(p);
+        CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(h->ev[2], st));
     h->last_stream = st;
     h->launched = true;

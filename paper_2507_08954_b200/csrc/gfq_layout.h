@@ -17,7 +17,11 @@ namespace gfq {
 enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
 
 // per-device int fields
-enum { DV_OUT = 0, DV_EFFD, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_HROK, DV_NI };
+enum { DV_OUT = 0, DV_EFFD, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_HROK, DV_RUN_EQ,
+       DV_DMAX, DV_POOLMAX, DV_POOLON, DV_DYN, DV_CACHE_N, DV_INSTDIRTY, DV_NI = 16 };
+// per-device double fields: state, then a copy of the device's DeviceConfig
+enum { DD_UAVG = 0, DD_INST, DD_LASTU, DD_CACHE_U, DD_CACHE_AVG, DD_MEMCAP, DD_THR, DD_PCIE,
+       DD_BETA, DD_WINDOW, DD_OVERLAP, DD_INVDMAX, DD_ND = 12 };
 
 // event kinds (engine.py:20-23)
 enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };
@@ -34,7 +38,7 @@ struct Layout {
     int32_t o_pt, o_ph, o_infl, o_head, o_done, o_pend;  // i32[F]
     int32_t o_fst;                                       // u8[F]
     int32_t o_ev_t, o_ev_seq, o_ev_meta;                 // f64[E], u32[E], u32[E]
-    int32_t o_dvi, o_dvd;                                // i32[ND][8], f64[ND][2]
+    int32_t o_dvi, o_dvd;                                // i32[ND][DV_NI], f64[ND][DD_ND]
     int32_t o_smp_t, o_smp_u;                            // f64[ND][S]
     int32_t o_run_i, o_run_d;                            // i32[ND][R][4], f64[ND][R][2]
     int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
@@ -96,7 +100,7 @@ inline void layout_finish(Layout& L) {
     L.o_head = take(4 * F); L.o_done = take(4 * F); L.o_pend = take(4 * F);
     L.o_fst = take(F);
     L.o_ev_t = take(8 * E); L.o_ev_seq = take(4 * E); L.o_ev_meta = take(4 * E);
-    L.o_dvi = take(4 * 8 * ND); L.o_dvd = take(8 * 2 * ND);
+    L.o_dvi = take(4 * DV_NI * ND); L.o_dvd = take(8 * DD_ND * ND);
     L.o_smp_t = take(8 * ND * S); L.o_smp_u = take(8 * ND * S);
     L.o_run_i = take(4 * 4 * ND * R); L.o_run_d = take(8 * 2 * ND * R);
     L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);

@@ -122,6 +122,7 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 // ------------------------------------------------------------------------
 // the per-warp simulation
 
+template <bool G>
 struct WarpSim {
     const Params& P;
     unsigned char* const sm;   // this warp's shared-memory slice
@@ -144,8 +145,9 @@ struct WarpSim {
     FI double* ev_t() const { return (double*)(sm + P.L.o_ev_t); }
     FI uint32_t* ev_seq() const { return (uint32_t*)(sm + P.L.o_ev_seq); }
     FI uint32_t* ev_meta() const { return (uint32_t*)(sm + P.L.o_ev_meta); }
-    FI int& DV(int d, int k) const { return ((int*)(sm + P.L.o_dvi))[d * 8 + k]; }
-    FI double& UAVG(int d) const { return ((double*)(sm + P.L.o_dvd))[d * 2]; }
+    FI int& DV(int d, int k) const { return ((int*)(sm + P.L.o_dvi))[d * DV_NI + k]; }
+    FI double& DD(int d, int k) const { return ((double*)(sm + P.L.o_dvd))[d * DD_ND + k]; }
+    FI double& UAVG(int d) const { return DD(d, DD_UAVG); }
     FI double& SMPT(int d, int i) const { return ((double*)(sm + P.L.o_smp_t))[d * P.L.S + i]; }
     FI double& SMPU(int d, int i) const { return ((double*)(sm + P.L.o_smp_u))[d * P.L.S + i]; }
     FI int& RI(int d, int r, int k) const { return ((int*)(sm + P.L.o_run_i))[(d * P.L.R + r) * 4 + k]; }
@@ -159,10 +161,16 @@ struct WarpSim {
     // ---- per-simulation inputs
     const gfq_sim* sim;
     int64_t toff, tb, roff;
+    bool tau_inc;
     const int* foff;
     int n, nf, ndev;
     int policy;
-    bool scripted, mqfq, fcfs;
+    bool scripted_, mqfq_, fcfs_;
+    // G = generic build (every policy, the scripted token provider, audit and
+    // event logs); !G = the MQFQ-Sticky / DeviceSet build the sweeps run
+#define SCRIPTED (G && scripted_)
+#define MQFQ (!G || mqfq_)
+#define FCFS (G && fcfs_)
     double T, alpha, dttl, period;
 
     FI double arr(int i) const { return P.arrival[toff + i]; }
@@ -172,7 +180,6 @@ struct WarpSim {
     FI double mem(int f) const { return P.mem[tb + f]; }
     FI double share(int f) const { return P.share[tb + f]; }
     FI double weight(int f) const { return P.weight[tb + f]; }
-    FI const gfq_device_cfg& dc(int d) const { return P.dcfg[sim->device_cfg + d]; }
 
     // ---- uniform scalar state (registers)
     double now, gvt;
@@ -249,7 +256,7 @@ struct WarpSim {
     // device model (device.py)
 
     FI int container_state(int d, int fn) const {         // device.py:104-112
-        if (!dc(d).pool_enabled) return GFQ_COLD;
+        if (!DV(d, DV_POOLON)) return GFQ_COLD;
         if (CNT(d, 0, fn) > 0) return GFQ_GPU_WARM;
         if (CNT(d, 1, fn) > 0) return GFQ_HOST_WARM;
         return GFQ_COLD;
@@ -315,7 +322,7 @@ struct WarpSim {
     FI bool admit_memory(int d, int fn) {
         if (CNT(d, 0, fn) > 0) return true;               // idle GPU_WARM exists
         double needed = mem(fn);
-        double free_mb = dc(d).mem_capacity_mb - resident_mb(d);
+        double free_mb = DD(d, DD_MEMCAP) - resident_mb(d);
         if (free_mb >= needed) return true;
         int np = DV(d, DV_NP);
         int nsw = 0;
@@ -367,7 +374,7 @@ struct WarpSim {
 
     // (C): every device refuses whatever the function
     FI bool certain_refusal() const {
-        if (scripted) return false;
+        if (SCRIPTED) return false;
         for (int d = 0; d < ndev; d++) if (token_free(d)) return false;
         return true;
     }
@@ -388,7 +395,7 @@ struct WarpSim {
     // order, first grant wins.  A refusal leaves a device unchanged, so the
     // order is re-derived by repeated minimum selection.
     FI int provider_assign(int fn, int& st) {
-        if (scripted) {
+        if (SCRIPTED) {
             s_att += 1;
             if (sim->scripted_deny_every && s_att % sim->scripted_deny_every == 0) return -1;
             if (s_out >= sim->scripted_d) return -1;
@@ -412,7 +419,7 @@ struct WarpSim {
     }
 
     FI int max_effective_d() const {                      // device.py:317-318
-        if (scripted) return sim->scripted_d;
+        if (SCRIPTED) return sim->scripted_d;
         int m = DV(0, DV_EFFD);
         for (int i = 1; i < ndev; i++) m = max(m, DV(i, DV_EFFD));
         return m;
@@ -428,6 +435,7 @@ struct WarpSim {
         DV(d, DV_NRUN) = nr + 1;
         __syncwarp();
         ust(CNT(d, 2, fn), (uint16_t)(CNT(d, 2, fn) + 1));
+        if (!SCRIPTED) ust(DV(d, DV_INSTDIRTY), 1);
     }
     FI bool run_remove(int d, int inv, double& duration, double& pure, int& st) {
         int nr = DV(d, DV_NRUN);
@@ -444,25 +452,27 @@ struct WarpSim {
         }
         ust(DV(d, DV_NRUN), nr - 1);
         ust(CNT(d, 2, fn), (uint16_t)(CNT(d, 2, fn) - 1));
+        if (!SCRIPTED) ust(DV(d, DV_INSTDIRTY), 1);
         return true;
     }
 
     // start_invocation, device.py:183-218
     FI void start_invocation(int d, int fn, int st, int inv, double& duration, double& pure) {
-        double base; int claimed = -1;
+        double base;
         if (st == GFQ_GPU_WARM) {
             base = warm(fn);
-            claimed = idle_entry(d, fn, GFQ_GPU_WARM);
         } else if (st == GFQ_HOST_WARM) {
-            double transfer = pymax(0.0, mem(fn) / dc(d).pcie_mb_per_s - dc(d).prefetch_overlap_s);
+            double transfer = pymax(0.0, mem(fn) / DD(d, DD_PCIE) - DD(d, DD_OVERLAP));
             base = warm(fn) + transfer;
-            claimed = idle_entry(d, fn, GFQ_HOST_WARM);
         } else {
             base = cold(fn);
         }
-        if (claimed >= 0) pool_erase(d, claimed);
+        if (st != GFQ_COLD) {            // claim the freshest idle container of that class
+            int claimed = idle_entry(d, fn, st);
+            if (claimed >= 0) pool_erase(d, claimed);
+        }
         int concurrent = DV(d, DV_NRUN) + 1;
-        double factor = 1.0 + dc(d).interference_beta * (double)(concurrent - 1);
+        double factor = 1.0 + DD(d, DD_BETA) * (double)(concurrent - 1);
         duration = base * factor;
         pure = warm(fn) * factor;
         run_append(d, inv, fn, st, duration, pure);
@@ -472,7 +482,7 @@ struct WarpSim {
     // (not spare, not evictable, last_used_s), first in list order on ties;
     // spare = another pooled container of the function exists and none runs
     FI void enforce_pool_cap(int d) {
-        int cap = dc(d).pool_max_containers;
+        int cap = DV(d, DV_POOLMAX);
         for (;;) {
             int np = DV(d, DV_NP), nr = DV(d, DV_NRUN);
             if (!(np + nr > cap && np > 0)) break;
@@ -495,7 +505,7 @@ struct WarpSim {
     FI bool device_complete(int d, int inv, int fn, double& duration, double& pure, int& st) {
         if (!run_remove(d, inv, duration, pure, st)) return false;
         ust(DV(d, DV_OUT), DV(d, DV_OUT) - 1);
-        if (!dc(d).pool_enabled) return true;
+        if (!DV(d, DV_POOLON)) return true;
         int np = DV(d, DV_NP);
         if (np >= P.L.P) { fail(GFQ_SIM_POOL_OVERFLOW); return false; }
         // the re-pooled entry is (fn, GPU_WARM, mem[fn], now, evictable=False)
@@ -517,33 +527,53 @@ struct WarpSim {
         return pymin(1.0, ps_val(a));
     }
 
-    // monitor_tick, device.py:282-297 -> effective_d; inst = the util sample
+    // monitor_tick, device.py:282-297 -> effective_d; inst = the util sample.
+    // instantaneous_util is cached per device (it only changes when the
+    // running set does).  The window average is a builtin Neumaier sum in
+    // window order; when every sample in the window equals the newest one
+    // and the (value, count) pair matches the last such computation the
+    // result is the same sequence of operations, so it is reused.
     FI int monitor_tick(int d, double& inst) {
-        double util = instantaneous_util(d);
+        double util = DD(d, DD_INST);
+        if (DV(d, DV_INSTDIRTY)) {              // the running set changed since the last tick
+            util = instantaneous_util(d);
+            __syncwarp();
+            DD(d, DD_INST) = util; DV(d, DV_INSTDIRTY) = 0;
+            __syncwarp();
+        }
         inst = util;
         const int S = P.L.S;
         int head = DV(d, DV_SHEAD), ns = DV(d, DV_SN);
         if (ns >= S) { fail(GFQ_SIM_SAMPLE_OVERFLOW); return DV(d, DV_EFFD); }
         int w = head + ns; if (w >= S) w -= S;
+        int run_eq = (ns > 0 && util == DD(d, DD_LASTU)) ? DV(d, DV_RUN_EQ) + 1 : 1;
         __syncwarp();
         SMPT(d, w) = now; SMPU(d, w) = util;
         __syncwarp();
         ns++;
-        double horizon = now - dc(d).util_window_s;
+        double horizon = now - DD(d, DD_WINDOW);
         while (ns > 0 && SMPT(d, head) <= horizon) { head++; if (head >= S) head = 0; ns--; }
-        PySum a; ps_init(a);
-        int j = head;
-        for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
-        double avg = ps_val(a) / (double)ns;
+        double avg;
+        bool uniform = run_eq >= ns;
+        if (uniform && DV(d, DV_CACHE_N) == ns && DD(d, DD_CACHE_U) == util) {
+            avg = DD(d, DD_CACHE_AVG);
+        } else {
+            PySum a; ps_init(a);
+            int j = head;
+            for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
+            avg = ps_val(a) / (double)ns;
+        }
         int effd = DV(d, DV_EFFD);
-        const gfq_device_cfg& c = dc(d);
-        if (!c.dynamic_d) effd = c.d_max;
-        else if (avg > c.util_threshold) effd = max(effd - 1, 1);
-        else if (avg < c.util_threshold - 1.0 / (double)c.d_max) effd = min(effd + 1, c.d_max);
-        int hrok = !(avg + 1.0 / (double)c.d_max > c.util_threshold);   // device.py:137-139
+        const int dmax = DV(d, DV_DMAX);
+        const double thr = DD(d, DD_THR), inv = DD(d, DD_INVDMAX);
+        if (!DV(d, DV_DYN)) effd = dmax;
+        else if (avg > thr) effd = max(effd - 1, 1);
+        else if (avg < thr - inv) effd = min(effd + 1, dmax);
+        int hrok = !(avg + inv > thr);                                  // device.py:137-139
         __syncwarp();
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
-        DV(d, DV_HROK) = hrok;
+        DV(d, DV_HROK) = hrok; DV(d, DV_RUN_EQ) = run_eq; DD(d, DD_LASTU) = util;
+        if (uniform) { DV(d, DV_CACHE_N) = ns; DD(d, DD_CACHE_U) = util; DD(d, DD_CACHE_AVG) = avg; }
         __syncwarp();
         return effd;
     }
@@ -568,9 +598,9 @@ struct WarpSim {
     // unstall, mqfq.py:129-139 (same backlogged set, ignoring the raise rule)
     FI void unstall() {
         if (tot_infl > 0) return;
-        double g0 = gvt;
-        recompute_gvt();              // refreshes gmin if needed; undo its max()
-        gvt = g0;
+        // the failed dispatch() that precedes every unstall (engine.py:177-181)
+        // left the cached minimum valid
+        if (!gmin_ok) { fail(GFQ_SIM_BAD_CONFIG); return; }
         if (gmin == ~0ull) return;
         double mv = from_key(gmin);
         if (gvt < mv) gvt = mv;
@@ -590,7 +620,7 @@ struct WarpSim {
             if (pt()[f] - done()[f] != 0) continue;          // backlogged
             double le = lex()[f], tt = ttl(f);
             if (now - le >= tt) {
-                fst()[f] = (uint8_t)(s | FL_INACTIVE | (scripted ? 0 : FL_NEWLY));
+                fst()[f] = (uint8_t)(s | FL_INACTIVE | (SCRIPTED ? 0 : FL_NEWLY));
                 newly = true;
             } else {
                 u64 k = okey(expiry_lb(le, tt));
@@ -598,7 +628,7 @@ struct WarpSim {
             }
         }
         __syncwarp();
-        if (wor32(newly) && !scripted) any_newly = true;
+        if (wor32(newly) && !SCRIPTED) any_newly = true;
         u64 m = wmin64(lbk);
         idle_lb = m == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_key(m);
     }
@@ -660,21 +690,21 @@ struct WarpSim {
     FI int dispatch_once(int& fn_out, int& dev_out, int& st_out) {
         n_calls++;
         int fn = -1;
-        if (mqfq) {
+        if (MQFQ) {
             recompute_gvt();
             refresh_states();
-            if (!certain_refusal()) fn = mqfq_candidate();
-        } else if (!certain_refusal()) {
-            if (fcfs) fn = fcfs_head < cursor ? flw(fcfs_head) : -1;   // policies.py:129-139
-            else if (policy == GFQ_POLICY_BATCH) fn = batch_candidate();
-            else fn = sjf_candidate();
+            if (tot_pend > 0 && !certain_refusal()) fn = mqfq_candidate();
+        } else if (tot_pend > 0 && !certain_refusal()) {
+            if (FCFS) fn = fcfs_head < cursor ? flw(fcfs_head) : -1;   // policies.py:129-139
+            else if (G && policy == GFQ_POLICY_BATCH) fn = batch_candidate();
+            else if (G) fn = sjf_candidate();
         }
         if (fn < 0) return -1;
         int st = 0;
         int dev = provider_assign(fn, st);
         if (dev < 0) return -1;
         int inv;
-        if (fcfs) {
+        if (FCFS) {
             inv = fcfs_head++;
             fcfs_infl++;
             audit_dispatch(inv, 0.0, 0.0, (cursor - fcfs_head) + 1, fcfs_infl);
@@ -686,16 +716,18 @@ struct WarpSim {
             int pe = pend()[fn] - 1, ninf = infl()[fn] + 1;
             double vt_before = vt()[fn];
             double nvt = vt_before;
-            if (mqfq) nvt = vt_before + tau()[fn] / weight(fn);          // mqfq.py:223
+            if (MQFQ) nvt = vt_before + tau()[fn] / weight(fn);          // mqfq.py:223
             __syncwarp();
             ph()[fn] = k; head()[fn] = nxt; pend()[fn] = pe; infl()[fn] = ninf;
-            if (mqfq) { vt()[fn] = nvt; lex()[fn] = now; }
+            if (MQFQ) { vt()[fn] = nvt; lex()[fn] = now; }
             __syncwarp();
-            if (policy == GFQ_POLICY_BATCH) draining = fn;
-            if (mqfq) {
+            if ((G && policy == GFQ_POLICY_BATCH)) draining = fn;
+            if (MQFQ) {
                 if (gmin_ok && nvt != vt_before && okey(vt_before) == gmin) gmin_ok = false;
                 audit_dispatch(inv, vt_before, gvt, pe + 1, ninf);
-                recompute_gvt();
+                // mqfq.py:238 recomputes the global VT here; _drain always calls
+                // dispatch() again next (engine.py:175-184), which recomputes it
+                // before any read, and nothing in between reads it: done there
             } else {
                 audit_dispatch(inv, 0.0, 0.0, pe + 1, ninf);
             }
@@ -715,20 +747,20 @@ struct WarpSim {
         if (!(s & FL_CREATED)) {                          // queue_for, mqfq.py:94-99
             s = FL_CREATED | FL_INACTIVE;
             v = 0.0;
-            le = mqfq ? now : 0.0;
+            le = MQFQ ? now : 0.0;
         }
         tot_pend++;
-        if (!fcfs) {
-            if (mqfq && (s & FL_INACTIVE)) {              // reactivation clamp, core.py:128-130
+        if (!FCFS) {
+            if (MQFQ && (s & FL_INACTIVE)) {              // reactivation clamp, core.py:128-130
                 v = pymax(v, gvt);
                 s &= (uint8_t)~FL_INACTIVE;
             }
             if (pe == 0) hd = inv;                        // pending.append
-            if (mqfq && p0 >= 1) {                        // iat.record(now - last_arrival)
+            if (MQFQ && p0 >= 1) {                        // iat.record(now - last_arrival)
                 double x = now - larr()[fn];
                 im = im + (x - im) / (double)p0;
             }
-            if (mqfq && p0 == d0 && gmin_ok) {            // (A) queue becomes backlogged
+            if (MQFQ && p0 == d0 && gmin_ok) {            // (A) queue becomes backlogged
                 u64 k = okey(v);
                 if (k < gmin) gmin = k;
             }
@@ -736,7 +768,7 @@ struct WarpSim {
         __syncwarp();
         fst()[fn] = s; pt()[fn] = p0 + 1; pend()[fn] = pe + 1;
         vt()[fn] = v; lex()[fn] = le; iat()[fn] = im; head()[fn] = hd;
-        if (mqfq) larr()[fn] = now;
+        if (MQFQ) larr()[fn] = now;
         __syncwarp();
     }
 
@@ -744,15 +776,15 @@ struct WarpSim {
     FI void policy_on_completion(int fn, double exec_s) {
         tot_infl--;
         int dn = done()[fn] + 1;
-        if (fcfs) { fcfs_infl -= 1; ust(done()[fn], dn); return; }
+        if (FCFS) { fcfs_infl -= 1; ust(done()[fn], dn); return; }
         int inf = infl()[fn] - 1;
         double tm = tau()[fn];
         tm = tm + (exec_s - tm) / (double)dn;            // tau.count == completions
         __syncwarp();
         done()[fn] = dn; infl()[fn] = inf; tau()[fn] = tm;
-        if (mqfq) lex()[fn] = now;
+        if (MQFQ) lex()[fn] = now;
         __syncwarp();
-        if (mqfq && pt()[fn] == dn) {                     // queue drained (idle)
+        if (MQFQ && pt()[fn] == dn) {                     // queue drained (idle)
             if (gmin_ok && okey(vt()[fn]) == gmin) gmin_ok = false;          // (A)
             idle_lb = pymin(idle_lb, expiry_lb(now, ttl(fn)));               // (B)
         }
@@ -763,7 +795,7 @@ struct WarpSim {
 
     FI void backlog_audit(int fn, bool on) {
         int k = n_backlog++;
-        if ((P.outputs & GFQ_WANT_AUDIT) && lane == 0 && k < P.audit_backlog_cap) {
+        if ((G && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_backlog_cap) {
             int64_t o = (int64_t)sid * P.audit_backlog_cap + k;
             P.backlog_time[o] = now; P.backlog_meta[o] = (fn << 1) | (on ? 1 : 0);
         }
@@ -798,7 +830,7 @@ struct WarpSim {
     // _start, engine.py:187-197
     FI void start(int inv, int fn, int dev, int st) {
         double duration, pure;
-        if (scripted) {
+        if (SCRIPTED) {
             // drive(): completion at now + next(exec_iter) (oracles.py:235-236)
             duration = P.execs[sim->exec_off + (s_exec % sim->exec_len)];
             s_exec++;
@@ -825,7 +857,7 @@ struct WarpSim {
             int inv = dispatch_once(fn, dev, st);
             if (inv < 0) {
                 if (!retried && tot_infl == 0 && tot_pend > 0) {
-                    if (mqfq) unstall();
+                    if (MQFQ) unstall();
                     retried = true;
                     continue;
                 }
@@ -839,7 +871,7 @@ struct WarpSim {
 
     FI void on_arrival(int inv) {                         // engine.py:121-129
         int fn = flw(inv);
-        if (!scripted) {
+        if (!SCRIPTED) {
             if (pt()[fn] - done()[fn] == 0) backlog_audit(fn, true);   // _backlog_change(+1)
             if (fst()[fn] & FL_MARKED) {                   // unmark_evictable on every device
                 for (int d = 0; d < ndev; d++) {
@@ -853,19 +885,19 @@ struct WarpSim {
             }
         }
         policy_on_arrival(inv, fn);
-        if (!scripted && !tick_on) push(now + period, EV_TICK, 0);
+        if (!SCRIPTED && !tick_on) push(now + period, EV_TICK, 0);
     }
 
     FI void on_completion(int inv, int dev) {             // engine.py:131-153
         int fn = flw(inv);
         double duration = 0.0, pure = 0.0; int st = 0;
-        if (scripted) {
+        if (SCRIPTED) {
             s_out -= 1;
             if (!run_remove(0, inv, duration, pure, st)) return;
             policy_on_completion(fn, duration);
         } else {
             if (!device_complete(dev, inv, fn, duration, pure, st)) return;
-            policy_on_completion(fn, sim->tau_includes_overheads ? duration : pure);
+            policy_on_completion(fn, tau_inc ? duration : pure);
         }
         int k = n_comp++;
         if (lane == 0) {
@@ -877,9 +909,9 @@ struct WarpSim {
                 P.rec_order[roff + inv] = k;
             }
         }
-        if (!scripted && pt()[fn] - done()[fn] == 0) {     // _backlog_change(-1)
+        if (!SCRIPTED && pt()[fn] - done()[fn] == 0) {     // _backlog_change(-1)
             backlog_audit(fn, false);
-            if (mqfq) push(now + ttl(fn), EV_EXPIRY, (uint32_t)fn);
+            if (MQFQ) push(now + ttl(fn), EV_EXPIRY, (uint32_t)fn);
         }
     }
 
@@ -888,7 +920,7 @@ struct WarpSim {
             double inst;
             int eff = monitor_tick(d, inst);
             int k = n_util++;
-            if ((P.outputs & GFQ_WANT_AUDIT) && lane == 0 && k < P.audit_util_cap) {
+            if ((G && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_util_cap) {
                 int64_t o = (int64_t)sid * P.audit_util_cap + k;
                 P.util_rows[o * 3 + 0] = now; P.util_rows[o * 3 + 1] = inst;
                 P.util_rows[o * 3 + 2] = UAVG(d);
@@ -924,7 +956,7 @@ struct WarpSim {
 
     FI void log_event(double t, int kind, long long payload) {
         int k = n_evlog++;
-        if ((P.outputs & GFQ_WANT_EVENTS) && lane == 0 && k < P.event_log_cap) {
+        if ((G && (P.outputs & GFQ_WANT_EVENTS)) && lane == 0 && k < P.event_log_cap) {
             int64_t o = (int64_t)sid * P.event_log_cap + k;
             P.event_time[o] = t;
             P.event_meta[o] = (int64_t)((payload << 2) | kind);
@@ -935,7 +967,7 @@ struct WarpSim {
     FI void run() {
         long long max_events = sim->max_events > 0 ? sim->max_events : 64ll * ((long long)n + 1024);
         double t_arr = n > 0 ? arr(0) : 0.0;
-        const bool early = P.early_exit && !(P.outputs & GFQ_WANT_EVENTS);
+        const bool early = P.early_exit && !(G && (P.outputs & GFQ_WANT_EVENTS));
         for (;;) {
             bool has_arr = cursor < n;
             if (!pmin_ok) pool_min();
@@ -984,9 +1016,12 @@ struct WarpSim {
             if (status) break;
             if (dr) drain();
             if (status) break;
-            if (!scripted) swap_out_inactive();
+            if (!SCRIPTED) swap_out_inactive();
         }
     }
 };
 
+#undef SCRIPTED
+#undef MQFQ
+#undef FCFS
 }  // namespace gfq

@@ -69,3 +69,21 @@ def test_early_exit_is_exact(engine, full_run):
         for k in ("dispatch", "records", "exec", "util", "backlog", "summary", "per_function",
                   "transcript"):
             assert a.get(k) == b.get(k), (c["name"], k)
+
+
+def test_fast_build_matches_reference(engine):
+    """MQFQ-Sticky / DeviceSet sims run the specialised k_sim<false> build
+    (bench configuration); its dispatch rows, records and statistics must
+    match the reference like the generic build's."""
+    from gpu_harness import compare_to_golden, run_cases
+    from paper_2507_08954_b200 import _abi
+    cases = [c for c in all_cases() if c.get("policy", "mqfq") == "mqfq" and not c.get("scripted")]
+    outs, _ = run_cases(cases, engine, early_exit=True,
+                        outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH)
+    gold = golden()
+    bad = {}
+    for c, o in zip(cases, outs):
+        m = compare_to_golden(o, gold[c["name"]], exact_keys=("dispatch", "records", "exec"))
+        if m:
+            bad[c["name"]] = m
+    assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
