@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--seeds", type=int, default=0, help="seeds per GPU (default: the config's)")
     return ap.parse_args()
 
 
@@ -228,7 +229,7 @@ def run_gfq(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = sweep.build(args.workload, rank)
+    w = sweep.build(args.workload, rank, **({"n_seeds": args.seeds} if args.seeds else {}))
     eng = Engine(local)
     w.upload(eng)
     outputs = _abi.WANT_STATS | _abi.WANT_HIST
@@ -258,7 +259,10 @@ def run_gfq(args):
     calls_per_step = int(counters[:, 1].sum())
     events_per_step = int(counters[:, 0].sum())
     scans = {"gvt_scans": int(counters[:, 5].sum()), "refresh_scans": int(counters[:, 6].sum()),
-             "candidate_scans": int(counters[:, 7].sum()),
+             "candidate_scans": int(counters[:, 7].sum()), "ticks": int(counters[:, 8].sum()),
+             "window_memo_hits": int(counters[:, 9].sum()),
+             "window_memo_misses": int(counters[:, 10].sum()),
+             "quiet_drains": int(counters[:, 11].sum()),
              "max_dynamic_events": int(counters[:, 4].max())}
 
     # ---- timed region (device time, CUDA events on the launch stream)

@@ -139,7 +139,7 @@ typedef struct gfq_launch_cfg {
     int32_t  reserved;
 } gfq_launch_cfg;
 
-#define GFQ_NCOUNTERS 8
+#define GFQ_NCOUNTERS 12
 
 /* Output ids for gfq_output_info / gfq_output_copy / gfq_output_device_ptr.
  * Per-sim arrays have n_sims elements; per-flow arrays are concatenated per
@@ -150,7 +150,9 @@ enum gfq_output_id {
     GFQ_OUT_COUNTERS,          /* int64  [sims][GFQ_NCOUNTERS]: events, dispatch()
                                   calls, dispatches, util rows, peak dynamic
                                   events, global-VT scans, keep-alive refresh
-                                  scans, candidate scans                        */
+                                  scans, candidate scans, monitor ticks,
+                                  window-average memo hits, misses, quiet
+                                  drains                                        */
     GFQ_OUT_FINAL_TIME,        /* double [sims]  simulated clock at exit          */
     GFQ_OUT_SUMMARY,           /* double [sims][3]: weighted_avg_latency_s,
                                   cold_hit_pct, mean_util (metrics.py:229-245)   */

@@ -15,7 +15,7 @@ GPU_WARM, HOST_WARM, COLD = 0, 1, 2
 EV_ARRIVAL, EV_COMPLETION, EV_MONITOR_TICK, EV_QUEUE_EXPIRY = 0, 1, 2, 3
 DEVMODEL_DEVICESET, DEVMODEL_SCRIPTED = 0, 1
 MAX_DEVICES = 8
-NCOUNTERS = 8
+NCOUNTERS = 12
 
 SIM_STATUS = {
     0: "ok",

@@ -215,7 +215,9 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
                 dvd[DD_WINDOW] = c.util_window_s; dvd[DD_OVERLAP] = c.prefetch_overlap_s;
                 dvd[DD_INVDMAX] = 1.0 / (double)c.d_max;
                 dvi[DV_HROK] = !(0.0 + dvd[DD_INVDMAX] > c.util_threshold);
-                dvi[DV_CACHE_N] = -1;
+                dvi[DV_INSTDIRTY] = 1;                // intern the idle utilization 0.0
+                u64* wk = (u64*)(base + p.L.o_wkey) + d * WMEMO;
+                for (int k = 0; k < WMEMO; k++) wk[k] = ~0ull;   // no valid key has all bits set
             }
         }
         __syncwarp();
@@ -239,6 +241,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
     w.n_events = 0;
     w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
     w.max_ev = w.n_gscan = w.n_rscan = w.n_cscan = 0;
+    w.n_ticks = w.n_whit = w.n_wmiss = w.n_quiet = 0;
     ps_init(w.util_sum);
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
@@ -253,6 +256,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
         int64_t* c = p.counters + (int64_t)sid * GFQ_NCOUNTERS;
         c[C_EVENTS] = w.n_events; c[C_CALLS] = w.n_calls; c[C_DISP] = w.n_disp; c[C_UTIL] = w.n_util;
         c[C_MAXEV] = w.max_ev; c[C_GSCAN] = w.n_gscan; c[C_RSCAN] = w.n_rscan; c[C_CSCAN] = w.n_cscan;
+        c[C_TICKS] = w.n_ticks; c[C_WHIT] = w.n_whit; c[C_WMISS] = w.n_wmiss; c[C_QUIET] = w.n_quiet;
         p.final_time[sid] = w.now;
         if (p.outputs & GFQ_WANT_AUDIT) p.backlog_count[sid] = w.n_backlog;
         if (p.outputs & GFQ_WANT_EVENTS) p.event_count[sid] = w.n_evlog;

@@ -117,7 +117,8 @@ FI uint32_t pm_make(int fn, int th, int ev) {
     return (uint32_t)fn | ((uint32_t)th << 24) | ((uint32_t)ev << 26);
 }
 
-enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN };
+enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN, C_TICKS,
+       C_WHIT, C_WMISS, C_QUIET };
 
 // ------------------------------------------------------------------------
 // the per-warp simulation
@@ -154,6 +155,9 @@ struct WarpSim {
     FI double& RD(int d, int r, int k) const { return ((double*)(sm + P.L.o_run_d))[(d * P.L.R + r) * 2 + k]; }
     FI uint32_t& PM(int d, int i) const { return ((uint32_t*)(sm + P.L.o_pool_m))[d * P.L.P + i]; }
     FI double& PT(int d, int i) const { return ((double*)(sm + P.L.o_pool_t))[d * P.L.P + i]; }
+    FI double& WDICTV(int d, int i) const { return ((double*)(sm + P.L.o_wdict))[d * WDICT + i]; }
+    FI u64& WKEY(int d, int i) const { return ((u64*)(sm + P.L.o_wkey))[d * WMEMO + i]; }
+    FI double& WVAL(int d, int i) const { return ((double*)(sm + P.L.o_wval))[d * WMEMO + i]; }
     FI uint16_t& CNT(int d, int kind, int f) const {   // kind: 0 gpu-warm, 1 host-warm, 2 running
         return ((uint16_t*)(sm + P.L.o_cnt))[(d * 3 + kind) * P.L.F + f];
     }
@@ -197,6 +201,7 @@ struct WarpSim {
     double idle_lb;                    // (B) no keep-alive can expire before this
     long long n_events;
     int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog, max_ev, n_gscan, n_rscan, n_cscan;
+    int n_ticks, n_whit, n_wmiss, n_quiet;
     PySum util_sum;
 
     FI WarpSim(const Params& p, unsigned char* s, int l, int id) : P(p), sm(s), lane(l), sid(id) {}
@@ -228,6 +233,7 @@ struct WarpSim {
 
     FI void pool_min() {                                  // lane-parallel argmin
         u64 bt = ~0ull; uint32_t bs = 0xffffffffu; int bslot = -1;
+        #pragma unroll 1
         for (int i = lane; i < nev; i += 32) {
             u64 k = okey(ev_t()[i]); uint32_t s = ev_seq()[i];
             if (k < bt || (k == bt && s < bs)) { bt = k; bs = s; bslot = i; }
@@ -267,6 +273,7 @@ struct WarpSim {
     FI int idle_entry(int d, int fn, int th) {
         int np = DV(d, DV_NP);
         u64 bk = ~0ull; int bi = 0x7fffffff;
+        #pragma unroll 1
         for (int i = lane; i < np; i += 32) {
             uint32_t m = PM(d, i);
             if (pm_fn(m) == fn && pm_th(m) == th) {
@@ -283,6 +290,7 @@ struct WarpSim {
     FI void pool_erase(int d, int i) {
         int np = DV(d, DV_NP);
         uint32_t m = PM(d, i);
+        #pragma unroll 1
         for (int base = i; base < np - 1; base += 32) {
             int j = base + lane;
             uint32_t mm = 0; double tt = 0.0;
@@ -301,11 +309,13 @@ struct WarpSim {
     FI double resident_mb(int d) {
         int np = DV(d, DV_NP);
         PySum a; ps_init(a);
+        #pragma unroll 1
         for (int base = 0; base < np; base += 32) {
             int i = base + lane;
             double v = 0.0; bool g = false;
             if (i < np) { uint32_t m = PM(d, i); g = pm_th(m) == GFQ_GPU_WARM; if (g) v = mem(pm_fn(m)); }
             unsigned gm = __ballot_sync(FULLMASK, g);
+            #pragma unroll 1
             while (gm) {
                 int j = __ffs(gm) - 1; gm &= gm - 1;
                 ps_add(a, __shfl_sync(FULLMASK, v, j));
@@ -313,6 +323,7 @@ struct WarpSim {
         }
         PySum b; ps_init(b);
         int nr = DV(d, DV_NRUN);
+        #pragma unroll 1
         for (int r = 0; r < nr; r++) ps_add(b, mem(RI(d, r, 1)));
         return ps_val(a) + ps_val(b);
     }
@@ -326,8 +337,10 @@ struct WarpSim {
         if (free_mb >= needed) return true;
         int np = DV(d, DV_NP);
         int nsw = 0;
+        #pragma unroll 1
         while (free_mb < needed) {
             u64 bk = ~0ull; int bi = 0x7fffffff;
+            #pragma unroll 1
             for (int i = lane; i < np; i += 32) {
                 uint32_t m = PM(d, i);
                 if (pm_th(m) == GFQ_GPU_WARM && !pm_sw(m)) {
@@ -345,10 +358,12 @@ struct WarpSim {
         }
         bool ok = free_mb >= needed;
         if (nsw) {   // commit (-> HOST_WARM) or roll back, one entry at a time
+            #pragma unroll 1
             for (int base = 0; base < np; base += 32) {
                 int i = base + lane;
                 bool s = i < np && pm_sw(PM(d, i));
                 unsigned smk = __ballot_sync(FULLMASK, s);
+                #pragma unroll 1
                 while (smk) {
                     int j = __ffs(smk) - 1; smk &= smk - 1;
                     int idx = base + j;
@@ -375,6 +390,7 @@ struct WarpSim {
     // (C): every device refuses whatever the function
     FI bool certain_refusal() const {
         if (SCRIPTED) return false;
+        #pragma unroll 1
         for (int d = 0; d < ndev; d++) if (token_free(d)) return false;
         return true;
     }
@@ -404,8 +420,10 @@ struct WarpSim {
             return 0;
         }
         unsigned tried = 0;
+        #pragma unroll 1
         for (int k = 0; k < ndev; k++) {
             int best = 0; int bkey = 0x7fffffff;
+            #pragma unroll 1
             for (int d = 0; d < ndev; d++) {
                 if (tried & (1u << d)) continue;
                 int key = (container_state(d, fn) << 20) | (DV(d, DV_OUT) << 4) | d;
@@ -421,6 +439,7 @@ struct WarpSim {
     FI int max_effective_d() const {                      // device.py:317-318
         if (SCRIPTED) return sim->scripted_d;
         int m = DV(0, DV_EFFD);
+        #pragma unroll 1
         for (int i = 1; i < ndev; i++) m = max(m, DV(i, DV_EFFD));
         return m;
     }
@@ -440,10 +459,12 @@ struct WarpSim {
     FI bool run_remove(int d, int inv, double& duration, double& pure, int& st) {
         int nr = DV(d, DV_NRUN);
         int ri = -1;
+        #pragma unroll 1
         for (int r = 0; r < nr; r++) if (RI(d, r, 0) == inv) { ri = r; break; }
         if (ri < 0) { fail(GFQ_SIM_BAD_CONFIG); return false; }   // RuntimeError
         int fn = RI(d, ri, 1);
         st = RI(d, ri, 2); duration = RD(d, ri, 0); pure = RD(d, ri, 1);
+        #pragma unroll 1
         for (int r = ri; r < nr - 1; r++) {
             int a = RI(d, r + 1, 0), b = RI(d, r + 1, 1), c = RI(d, r + 1, 2);
             double x = RD(d, r + 1, 0), y = RD(d, r + 1, 1);
@@ -483,10 +504,12 @@ struct WarpSim {
     // spare = another pooled container of the function exists and none runs
     FI void enforce_pool_cap(int d) {
         int cap = DV(d, DV_POOLMAX);
+        #pragma unroll 1
         for (;;) {
             int np = DV(d, DV_NP), nr = DV(d, DV_NRUN);
             if (!(np + nr > cap && np > 0)) break;
             unsigned bk01 = 0xffffffffu; u64 bk2 = ~0ull; int bi = 0x7fffffff;
+            #pragma unroll 1
             for (int i = lane; i < np; i += 32) {
                 uint32_t m = PM(d, i); int f = pm_fn(m);
                 bool spare = (int)CNT(d, 0, f) + (int)CNT(d, 1, f) > 1 && CNT(d, 2, f) == 0;
@@ -523,6 +546,7 @@ struct WarpSim {
     FI double instantaneous_util(int d) const {
         PySum a; ps_init(a);
         int nr = DV(d, DV_NRUN);
+        #pragma unroll 1
         for (int r = 0; r < nr; r++) ps_add(a, share(RI(d, r, 1)));
         return pymin(1.0, ps_val(a));
     }
@@ -530,15 +554,21 @@ struct WarpSim {
     // monitor_tick, device.py:282-297 -> effective_d; inst = the util sample.
     // instantaneous_util is cached per device (it only changes when the
     // running set does).  The window average is a builtin Neumaier sum in
-    // window order; when every sample in the window equals the newest one
-    // and the (value, count) pair matches the last such computation the
-    // result is the same sequence of operations, so it is reused.
+    // window order; it is memoised exactly: each device interns its distinct
+    // sample values (<= WDICT) as 4-bit ids, the window is the shift register
+    // of the ids of its samples, and (ids, count) fixes the summed sequence.
     FI int monitor_tick(int d, double& inst) {
         double util = DD(d, DD_INST);
+        int id = DV(d, DV_INSTID);
         if (DV(d, DV_INSTDIRTY)) {              // the running set changed since the last tick
             util = instantaneous_util(d);
+            int nd = DV(d, DV_WDICT_N);
+            id = 0;
+            #pragma unroll 1
+            for (int i = 0; i < nd; i++) if (WDICTV(d, i) == util) { id = i + 1; break; }
             __syncwarp();
-            DD(d, DD_INST) = util; DV(d, DV_INSTDIRTY) = 0;
+            if (id == 0 && nd < WDICT) { WDICTV(d, nd) = util; DV(d, DV_WDICT_N) = nd + 1; id = nd + 1; }
+            DD(d, DD_INST) = util; DV(d, DV_INSTDIRTY) = 0; DV(d, DV_INSTID) = id;
             __syncwarp();
         }
         inst = util;
@@ -546,22 +576,33 @@ struct WarpSim {
         int head = DV(d, DV_SHEAD), ns = DV(d, DV_SN);
         if (ns >= S) { fail(GFQ_SIM_SAMPLE_OVERFLOW); return DV(d, DV_EFFD); }
         int w = head + ns; if (w >= S) w -= S;
-        int run_eq = (ns > 0 && util == DD(d, DD_LASTU)) ? DV(d, DV_RUN_EQ) + 1 : 1;
+        u64 code = ((u64)__double_as_longlong(DD(d, DD_WCODE)) << 4) | (u64)id;
+        int zage = id ? min(DV(d, DV_ZAGE) + 1, 255) : 0;
         __syncwarp();
         SMPT(d, w) = now; SMPU(d, w) = util;
         __syncwarp();
         ns++;
         double horizon = now - DD(d, DD_WINDOW);
+        #pragma unroll 1
         while (ns > 0 && SMPT(d, head) <= horizon) { head++; if (head >= S) head = 0; ns--; }
         double avg;
-        bool uniform = run_eq >= ns;
-        if (uniform && DV(d, DV_CACHE_N) == ns && DD(d, DD_CACHE_U) == util) {
-            avg = DD(d, DD_CACHE_AVG);
+        bool memo = ns <= 14 && zage >= ns;          // key ~0 stays the empty-slot marker
+        u64 key = 0; int slot = 0;
+        if (memo) {
+            key = (code & ((1ull << (4 * ns)) - 1)) | ((u64)ns << 60);
+            slot = (int)((key * 0x9E3779B97F4A7C15ull) >> 60);
+        }
+        if (memo && WKEY(d, slot) == key) {
+            avg = WVAL(d, slot);
+            n_whit++;
         } else {
+            n_wmiss++;
             PySum a; ps_init(a);
             int j = head;
+            #pragma unroll 1
             for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
             avg = ps_val(a) / (double)ns;
+            if (memo) { __syncwarp(); WKEY(d, slot) = key; WVAL(d, slot) = avg; __syncwarp(); }
         }
         int effd = DV(d, DV_EFFD);
         const int dmax = DV(d, DV_DMAX);
@@ -572,8 +613,8 @@ struct WarpSim {
         int hrok = !(avg + inv > thr);                                  // device.py:137-139
         __syncwarp();
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
-        DV(d, DV_HROK) = hrok; DV(d, DV_RUN_EQ) = run_eq; DD(d, DD_LASTU) = util;
-        if (uniform) { DV(d, DV_CACHE_N) = ns; DD(d, DD_CACHE_U) = util; DD(d, DD_CACHE_AVG) = avg; }
+        DV(d, DV_HROK) = hrok; DV(d, DV_ZAGE) = zage;
+        DD(d, DD_WCODE) = __longlong_as_double((long long)code);
         __syncwarp();
         return effd;
     }
@@ -587,6 +628,7 @@ struct WarpSim {
         if (!gmin_ok) {
             n_gscan++;
             u64 bk = ~0ull;
+            #pragma unroll 1
             for (int f = lane; f < nf; f += 32)
                 if (pt()[f] - done()[f] > 0) { u64 k = okey(vt()[f]); if (k < bk) bk = k; }
             gmin = wmin64(bk);
@@ -614,6 +656,7 @@ struct WarpSim {
         n_rscan++;
         u64 lbk = ~0ull;
         bool newly = false;
+        #pragma unroll 1
         for (int f = lane; f < nf; f += 32) {
             uint8_t s = fst()[f];
             if ((s & (FL_CREATED | FL_INACTIVE)) != FL_CREATED) continue;
@@ -639,6 +682,7 @@ struct WarpSim {
         n_cscan++;
         bool use_inf = max_effective_d() != 1;
         u64 bk = ~0ull;
+        #pragma unroll 1
         for (int f = lane; f < nf; f += 32) {
             int pe = pend()[f];
             if (pe > 0 && vt()[f] - gvt <= T) {
@@ -659,6 +703,7 @@ struct WarpSim {
             return pend()[dr] == 0 ? -1 : dr;                // hold for late arrivals
         n_cscan++;
         unsigned bk = 0xffffffffu;
+        #pragma unroll 1
         for (int f = lane; f < nf; f += 32)
             if (pend()[f] > 0) bk = min(bk, (unsigned)head()[f]);
         unsigned m = wmin32(bk);
@@ -669,6 +714,7 @@ struct WarpSim {
     FI int sjf_candidate() {
         n_cscan++;
         u64 bk = ~0ull; int bf = 0x7fffffff;
+        #pragma unroll 1
         for (int f = lane; f < nf; f += 32)
             if (pend()[f] > 0) { u64 k = okey(tau()[f]); if (k < bk) { bk = k; bf = f; } }
         u64 m = wmin64(bk);
@@ -805,8 +851,10 @@ struct WarpSim {
     FI void swap_out_inactive() {
         if (!any_newly) return;
         any_newly = false;
+        #pragma unroll 1
         for (int d = 0; d < ndev; d++) {
             int np = DV(d, DV_NP);
+            #pragma unroll 1
             for (int i = lane; i < np; i += 32) {
                 uint32_t m = PM(d, i);
                 if (fst()[pm_fn(m)] & FL_NEWLY) {
@@ -817,9 +865,11 @@ struct WarpSim {
             }
         }
         __syncwarp();
+        #pragma unroll 1
         for (int f = lane; f < nf; f += 32) {
             uint8_t s = fst()[f];
             if (s & FL_NEWLY) {
+                #pragma unroll 1
                 for (int d = 0; d < ndev; d++) { CNT(d, 1, f) += CNT(d, 0, f); CNT(d, 0, f) = 0; }
                 fst()[f] = (uint8_t)((s & ~FL_NEWLY) | FL_MARKED);
             }
@@ -850,8 +900,21 @@ struct WarpSim {
 
     // _drain, engine.py:173-185 (the swap-out after the loop is done by the
     // caller, once per event)
+    // A drain whose single dispatch() call provably returns None and is not
+    // retried after unstall (engine.py:177-181): the global-VT recompute is
+    // idempotent (the cached minimum is valid and already applied), no
+    // keep-alive can expire yet (B), and either nothing is pending or every
+    // device refuses (C) while something is in flight.  Such a drain is one
+    // counted dispatch() call and no state change.
+    FI bool quiet_drain() const {
+        if (MQFQ && !(gmin_ok && now < idle_lb)) return false;
+        return tot_pend == 0 || (tot_infl > 0 && certain_refusal());
+    }
+
     FI void drain() {
+        if (quiet_drain()) { n_calls++; n_quiet++; return; }
         bool retried = false;
+        #pragma unroll 1
         for (;;) {
             int fn, dev, st;
             int inv = dispatch_once(fn, dev, st);
@@ -874,8 +937,10 @@ struct WarpSim {
         if (!SCRIPTED) {
             if (pt()[fn] - done()[fn] == 0) backlog_audit(fn, true);   // _backlog_change(+1)
             if (fst()[fn] & FL_MARKED) {                   // unmark_evictable on every device
+                #pragma unroll 1
                 for (int d = 0; d < ndev; d++) {
                     int np = DV(d, DV_NP);
+                    #pragma unroll 1
                     for (int i = lane; i < np; i += 32) {
                         uint32_t m = PM(d, i);
                         if (pm_fn(m) == fn) PM(d, i) = m & ~(1u << 26);
@@ -916,6 +981,7 @@ struct WarpSim {
     }
 
     FI void on_monitor() {                                // engine.py:155-165
+        #pragma unroll 1
         for (int d = 0; d < ndev; d++) {
             double inst;
             int eff = monitor_tick(d, inst);
@@ -968,6 +1034,7 @@ struct WarpSim {
         long long max_events = sim->max_events > 0 ? sim->max_events : 64ll * ((long long)n + 1024);
         double t_arr = n > 0 ? arr(0) : 0.0;
         const bool early = P.early_exit && !(G && (P.outputs & GFQ_WANT_EVENTS));
+        #pragma unroll 1
         for (;;) {
             bool has_arr = cursor < n;
             if (!pmin_ok) pool_min();
@@ -996,6 +1063,7 @@ struct WarpSim {
                 on_arrival(inv);
             } else if (kind == EV_TICK) {
                 tick_on = false;
+                n_ticks++;
                 log_event(t, EV_TICK, -1);
                 on_monitor();
             } else {
