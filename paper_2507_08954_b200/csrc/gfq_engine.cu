@@ -165,9 +165,9 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
 }
 
 
-template <bool G>
+template <bool G, bool ND1>
 __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, int lane, int sid) {
-    WarpSim<G> w(p, base, lane, sid);
+    WarpSim<G, ND1> w(p, base, lane, sid);
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
     const int t = sim->trace;
@@ -220,7 +220,17 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
                 for (int k = 0; k < WMEMO; k++) wk[k] = ~0ull;   // no valid key has all bits set
             }
         }
+        uint32_t* dg = (uint32_t*)(base + p.L.o_diag);
+        if (lane < DG_N) dg[lane] = 0;
         __syncwarp();
+        if (ND1) {                                 // device 0's mutable state -> registers
+            const int* dvi = (const int*)(base + p.L.o_dvi);
+            const double* dvd = (const double*)(base + p.L.o_dvd);
+#pragma unroll
+            for (int k = 0; k < DV_NSTATE; k++) w.hv[k] = dvi[k];
+#pragma unroll
+            for (int k = 0; k < DD_NSTATE; k++) w.hd[k] = dvd[k];
+        }
     }
     w.period = 0.0;
     if (!scripted) {                                   // engine.py:80-81
@@ -240,8 +250,6 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
     w.idle_lb = __longlong_as_double(0x7ff0000000000000ll);
     w.n_events = 0;
     w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
-    w.max_ev = w.n_gscan = w.n_rscan = w.n_cscan = 0;
-    w.n_ticks = w.n_whit = w.n_wmiss = w.n_quiet = 0;
     ps_init(w.util_sum);
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
@@ -255,8 +263,10 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
         p.summary[(int64_t)sid * 3 + 2] = w.n_util ? ps_val(w.util_sum) / (double)w.n_util : 0.0;
         int64_t* c = p.counters + (int64_t)sid * GFQ_NCOUNTERS;
         c[C_EVENTS] = w.n_events; c[C_CALLS] = w.n_calls; c[C_DISP] = w.n_disp; c[C_UTIL] = w.n_util;
-        c[C_MAXEV] = w.max_ev; c[C_GSCAN] = w.n_gscan; c[C_RSCAN] = w.n_rscan; c[C_CSCAN] = w.n_cscan;
-        c[C_TICKS] = w.n_ticks; c[C_WHIT] = w.n_whit; c[C_WMISS] = w.n_wmiss; c[C_QUIET] = w.n_quiet;
+        const uint32_t* dg = (const uint32_t*)(base + p.L.o_diag);
+        c[C_MAXEV] = dg[DG_MAXEV]; c[C_GSCAN] = dg[DG_GSCAN]; c[C_RSCAN] = dg[DG_RSCAN];
+        c[C_CSCAN] = dg[DG_CSCAN]; c[C_TICKS] = dg[DG_TICKS]; c[C_WHIT] = dg[DG_WHIT];
+        c[C_WMISS] = dg[DG_WMISS]; c[C_QUIET] = dg[DG_QUIET];
         p.final_time[sid] = w.now;
         if (p.outputs & GFQ_WANT_AUDIT) p.backlog_count[sid] = w.n_backlog;
         if (p.outputs & GFQ_WANT_EVENTS) p.event_count[sid] = w.n_evlog;
@@ -272,7 +282,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
 #ifndef GFQ_MINB
 #define GFQ_MINB 4
 #endif
-template <bool G>
+template <bool G, bool ND1>
 __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ P
         if (lane == 0) idx = atomicAdd(p.work, 1);
         idx = __shfl_sync(FULLMASK, idx, 0);
         if (idx >= p.n_sims) break;
-        run_one<G>(p, base, lane, p.order[idx]);
+        run_one<G, ND1>(p, base, lane, p.order[idx]);
     }
 }
 
@@ -403,7 +413,7 @@ struct gfq_handle {
     gfq_launch_cfg cfg{};
     Layout L{};
     int wpb = 0, blocks = 0, rwpb = 4;
-    bool generic = true;
+    bool generic = true, nd1 = false;
     bool prepared = false;
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
@@ -662,7 +672,10 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     bool generic = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
     for (int i = 0; i < n_sims && !generic; i++)
         generic = sims[i].policy != GFQ_POLICY_MQFQ || sims[i].device_model != GFQ_DEVMODEL_DEVICESET;
-    const void* kfn = generic ? (const void*)k_sim<true> : (const void*)k_sim<false>;
+    bool nd1 = !generic;
+    for (int i = 0; i < n_sims && nd1; i++) nd1 = sims[i].n_devices == 1;
+    const void* kfn = generic ? (const void*)k_sim<true, false>
+                    : nd1 ? (const void*)k_sim<false, true> : (const void*)k_sim<false, false>;
     int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, 4) : 4;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
     size_t smem = (size_t)wpb * L.bytes;
@@ -745,6 +758,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->blocks = blocks;
     h->rwpb = rwpb;
     h->generic = generic;
+    h->nd1 = nd1;
     h->prepared = true;
     h->launched = false;
     return GFQ_OK;
@@ -815,8 +829,9 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(h->ev[0], st));
     if (h->n_sims > 0) {
         size_t smem = (size_t)h->wpb * h->L.bytes;
-        if (h->generic) k_sim<true><<<h->blocks, h->wpb * 32, smem, st>>>(p);
-        else k_sim<false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        if (h->generic) k_sim<true, false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        else if (h->nd1) k_sim<false, true><<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        else k_sim<false, false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[1], st));

@@ -17,15 +17,19 @@ namespace gfq {
 enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
 
 // per-device int fields
-enum { DV_OUT = 0, DV_EFFD, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_HROK, DV_RUN_EQ,
-       DV_DMAX, DV_POOLMAX, DV_POOLON, DV_DYN, DV_WDICT_N, DV_INSTDIRTY, DV_INSTID, DV_ZAGE,
-       DV_NI = 18 };
+enum { DV_OUT = 0, DV_EFFD, DV_HROK, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_INSTDIRTY, DV_INSTID,
+       DV_ZAGE, DV_WDICT_N, DV_NSTATE,                       // mutable state (registers
+       DV_DMAX = DV_NSTATE, DV_POOLMAX, DV_POOLON, DV_DYN,   //  in the 1-device build);
+       DV_NI = 16 };                                         //  DeviceConfig copy
 // per-device double fields: state, then a copy of the device's DeviceConfig
-enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_MEMCAP, DD_THR, DD_PCIE,
-       DD_BETA, DD_WINDOW, DD_OVERLAP, DD_INVDMAX, DD_ND = 10 };
+enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_NSTATE,
+       DD_MEMCAP = DD_NSTATE, DD_THR, DD_PCIE, DD_BETA, DD_WINDOW, DD_OVERLAP, DD_INVDMAX,
+       DD_ND = 10 };
 // window-average memo: WDICT distinct utilization values per device,
 // WMEMO direct-mapped (window code, count) -> average entries
 enum { WDICT = 15, WMEMO = 16 };
+// per-warp diagnostic counters (shared memory, lane 0 increments)
+enum { DG_MAXEV = 0, DG_GSCAN, DG_RSCAN, DG_CSCAN, DG_TICKS, DG_WHIT, DG_WMISS, DG_QUIET, DG_N };
 
 // event kinds (engine.py:20-23)
 enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };
@@ -48,6 +52,7 @@ struct Layout {
     int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
     int32_t o_cnt;                                       // u16[ND][3][F]: gpu-warm, host-warm, running
     int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u64[ND][WMEMO], f64[ND][WMEMO]
+    int32_t o_diag;                                      // u32[DG_N]
     int32_t bytes;                                       // slice size
 };
 
@@ -111,6 +116,7 @@ inline void layout_finish(Layout& L) {
     L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);
     L.o_cnt = take(2 * 3 * ND * F);
     L.o_wdict = take(8 * WDICT * ND); L.o_wkey = take(8 * WMEMO * ND); L.o_wval = take(8 * WMEMO * ND);
+    L.o_diag = take(4 * DG_N);
     L.bytes = o;
 }
 

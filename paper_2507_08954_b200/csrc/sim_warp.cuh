@@ -123,7 +123,7 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 // ------------------------------------------------------------------------
 // the per-warp simulation
 
-template <bool G>
+template <bool G, bool ND1>
 struct WarpSim {
     const Params& P;
     unsigned char* const sm;   // this warp's shared-memory slice
@@ -146,9 +146,19 @@ struct WarpSim {
     FI double* ev_t() const { return (double*)(sm + P.L.o_ev_t); }
     FI uint32_t* ev_seq() const { return (uint32_t*)(sm + P.L.o_ev_seq); }
     FI uint32_t* ev_meta() const { return (uint32_t*)(sm + P.L.o_ev_meta); }
-    FI int& DV(int d, int k) const { return ((int*)(sm + P.L.o_dvi))[d * DV_NI + k]; }
-    FI double& DD(int d, int k) const { return ((double*)(sm + P.L.o_dvd))[d * DD_ND + k]; }
-    FI double& UAVG(int d) const { return DD(d, DD_UAVG); }
+    // per-device fields; in the 1-device build the mutable ones are registers
+    int hv[DV_NSTATE]; double hd[DD_NSTATE];
+    FI int& DV(int d, int k) {
+        if (ND1 && k < DV_NSTATE) return hv[k];
+        return ((int*)(sm + P.L.o_dvi))[d * DV_NI + k];
+    }
+    FI double& DD(int d, int k) {
+        if (ND1 && k < DD_NSTATE) return hd[k];
+        return ((double*)(sm + P.L.o_dvd))[d * DD_ND + k];
+    }
+    FI int NDEV() const { return ND1 ? 1 : ndev; }
+    FI void diag(int k, unsigned v = 1) { if (lane == 0) ((uint32_t*)(sm + P.L.o_diag))[k] += v; }
+    FI double& UAVG(int d) { return DD(d, DD_UAVG); }
     FI double& SMPT(int d, int i) const { return ((double*)(sm + P.L.o_smp_t))[d * P.L.S + i]; }
     FI double& SMPU(int d, int i) const { return ((double*)(sm + P.L.o_smp_u))[d * P.L.S + i]; }
     FI int& RI(int d, int r, int k) const { return ((int*)(sm + P.L.o_run_i))[(d * P.L.R + r) * 4 + k]; }
@@ -200,8 +210,7 @@ struct WarpSim {
     bool gmin_ok; u64 gmin;            // (A) cached min okey(vt) over backlogged queues
     double idle_lb;                    // (B) no keep-alive can expire before this
     long long n_events;
-    int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog, max_ev, n_gscan, n_rscan, n_cscan;
-    int n_ticks, n_whit, n_wmiss, n_quiet;
+    int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog;
     PySum util_sum;
 
     FI WarpSim(const Params& p, unsigned char* s, int l, int id) : P(p), sm(s), lane(l), sid(id) {}
@@ -222,7 +231,7 @@ struct WarpSim {
         if (kind == EV_TICK) { tick_on = true; tick_t = t; tick_seq = s; return; }
         if (nev >= P.L.E) { fail(GFQ_SIM_EVENT_OVERFLOW); return; }
         int slot = nev++;
-        max_ev = max(max_ev, nev);
+        if (lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
         __syncwarp();
         ev_t()[slot] = t; ev_seq()[slot] = s; ev_meta()[slot] = ((uint32_t)kind << 30) | payload;
         __syncwarp();
@@ -261,7 +270,7 @@ struct WarpSim {
     // ==================================================================
     // device model (device.py)
 
-    FI int container_state(int d, int fn) const {         // device.py:104-112
+    FI int container_state(int d, int fn) {         // device.py:104-112
         if (!DV(d, DV_POOLON)) return GFQ_COLD;
         if (CNT(d, 0, fn) > 0) return GFQ_GPU_WARM;
         if (CNT(d, 1, fn) > 0) return GFQ_HOST_WARM;
@@ -382,16 +391,16 @@ struct WarpSim {
     }
 
     // the function-independent part of try_acquire_token (device.py:134-139)
-    FI bool token_free(int d) const {
+    FI bool token_free(int d) {
         int out = DV(d, DV_OUT);
         return out < DV(d, DV_EFFD) && (out == 0 || DV(d, DV_HROK));
     }
 
     // (C): every device refuses whatever the function
-    FI bool certain_refusal() const {
+    FI bool certain_refusal() {
         if (SCRIPTED) return false;
         #pragma unroll 1
-        for (int d = 0; d < ndev; d++) if (token_free(d)) return false;
+        for (int d = 0; d < NDEV(); d++) if (token_free(d)) return false;
         return true;
     }
 
@@ -421,10 +430,10 @@ struct WarpSim {
         }
         unsigned tried = 0;
         #pragma unroll 1
-        for (int k = 0; k < ndev; k++) {
+        for (int k = 0; k < NDEV(); k++) {
             int best = 0; int bkey = 0x7fffffff;
             #pragma unroll 1
-            for (int d = 0; d < ndev; d++) {
+            for (int d = 0; d < NDEV(); d++) {
                 if (tried & (1u << d)) continue;
                 int key = (container_state(d, fn) << 20) | (DV(d, DV_OUT) << 4) | d;
                 if (key < bkey) { bkey = key; best = d; }
@@ -436,11 +445,11 @@ struct WarpSim {
         return -1;
     }
 
-    FI int max_effective_d() const {                      // device.py:317-318
+    FI int max_effective_d() {                      // device.py:317-318
         if (SCRIPTED) return sim->scripted_d;
         int m = DV(0, DV_EFFD);
         #pragma unroll 1
-        for (int i = 1; i < ndev; i++) m = max(m, DV(i, DV_EFFD));
+        for (int i = 1; i < NDEV(); i++) m = max(m, DV(i, DV_EFFD));
         return m;
     }
 
@@ -543,7 +552,7 @@ struct WarpSim {
     }
 
     // instantaneous_util, device.py:279-280
-    FI double instantaneous_util(int d) const {
+    FI double instantaneous_util(int d) {
         PySum a; ps_init(a);
         int nr = DV(d, DV_NRUN);
         #pragma unroll 1
@@ -594,9 +603,9 @@ struct WarpSim {
         }
         if (memo && WKEY(d, slot) == key) {
             avg = WVAL(d, slot);
-            n_whit++;
+            diag(DG_WHIT);
         } else {
-            n_wmiss++;
+            diag(DG_WMISS);
             PySum a; ps_init(a);
             int j = head;
             #pragma unroll 1
@@ -626,7 +635,7 @@ struct WarpSim {
     // so the filter is "backlogged"; the minimum is cached (gmin).
     FI void recompute_gvt() {
         if (!gmin_ok) {
-            n_gscan++;
+            diag(DG_GSCAN);
             u64 bk = ~0ull;
             #pragma unroll 1
             for (int f = lane; f < nf; f += 32)
@@ -653,7 +662,7 @@ struct WarpSim {
     // become INACTIVE (and are queued for swap-out).
     FI void refresh_states() {
         if (now < idle_lb) return;
-        n_rscan++;
+        diag(DG_RSCAN);
         u64 lbk = ~0ull;
         bool newly = false;
         #pragma unroll 1
@@ -679,7 +688,7 @@ struct WarpSim {
     // candidates (mqfq.py:200-205) + the two stable sorts (mqfq.py:213-215):
     // lexicographic min of (in_flight if D != 1, -len(pending), name)
     FI int mqfq_candidate() {
-        n_cscan++;
+        diag(DG_CSCAN);
         bool use_inf = max_effective_d() != 1;
         u64 bk = ~0ull;
         #pragma unroll 1
@@ -701,7 +710,7 @@ struct WarpSim {
         int dr = draining;
         if (dr >= 0 && (pend()[dr] > 0 || infl()[dr] > 0))
             return pend()[dr] == 0 ? -1 : dr;                // hold for late arrivals
-        n_cscan++;
+        diag(DG_CSCAN);
         unsigned bk = 0xffffffffu;
         #pragma unroll 1
         for (int f = lane; f < nf; f += 32)
@@ -712,7 +721,7 @@ struct WarpSim {
 
     // SjfPolicy.dispatch, policies.py:245-262: min tau.mean, name order on ties
     FI int sjf_candidate() {
-        n_cscan++;
+        diag(DG_CSCAN);
         u64 bk = ~0ull; int bf = 0x7fffffff;
         #pragma unroll 1
         for (int f = lane; f < nf; f += 32)
@@ -840,6 +849,7 @@ struct WarpSim {
     // engine (engine.py)
 
     FI void backlog_audit(int fn, bool on) {
+        if (!G) return;
         int k = n_backlog++;
         if ((G && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_backlog_cap) {
             int64_t o = (int64_t)sid * P.audit_backlog_cap + k;
@@ -852,7 +862,7 @@ struct WarpSim {
         if (!any_newly) return;
         any_newly = false;
         #pragma unroll 1
-        for (int d = 0; d < ndev; d++) {
+        for (int d = 0; d < NDEV(); d++) {
             int np = DV(d, DV_NP);
             #pragma unroll 1
             for (int i = lane; i < np; i += 32) {
@@ -870,7 +880,7 @@ struct WarpSim {
             uint8_t s = fst()[f];
             if (s & FL_NEWLY) {
                 #pragma unroll 1
-                for (int d = 0; d < ndev; d++) { CNT(d, 1, f) += CNT(d, 0, f); CNT(d, 0, f) = 0; }
+                for (int d = 0; d < NDEV(); d++) { CNT(d, 1, f) += CNT(d, 0, f); CNT(d, 0, f) = 0; }
                 fst()[f] = (uint8_t)((s & ~FL_NEWLY) | FL_MARKED);
             }
         }
@@ -906,13 +916,13 @@ struct WarpSim {
     // keep-alive can expire yet (B), and either nothing is pending or every
     // device refuses (C) while something is in flight.  Such a drain is one
     // counted dispatch() call and no state change.
-    FI bool quiet_drain() const {
+    FI bool quiet_drain() {
         if (MQFQ && !(gmin_ok && now < idle_lb)) return false;
         return tot_pend == 0 || (tot_infl > 0 && certain_refusal());
     }
 
     FI void drain() {
-        if (quiet_drain()) { n_calls++; n_quiet++; return; }
+        if (quiet_drain()) { n_calls++; diag(DG_QUIET); return; }
         bool retried = false;
         #pragma unroll 1
         for (;;) {
@@ -938,7 +948,7 @@ struct WarpSim {
             if (pt()[fn] - done()[fn] == 0) backlog_audit(fn, true);   // _backlog_change(+1)
             if (fst()[fn] & FL_MARKED) {                   // unmark_evictable on every device
                 #pragma unroll 1
-                for (int d = 0; d < ndev; d++) {
+                for (int d = 0; d < NDEV(); d++) {
                     int np = DV(d, DV_NP);
                     #pragma unroll 1
                     for (int i = lane; i < np; i += 32) {
@@ -982,7 +992,7 @@ struct WarpSim {
 
     FI void on_monitor() {                                // engine.py:155-165
         #pragma unroll 1
-        for (int d = 0; d < ndev; d++) {
+        for (int d = 0; d < NDEV(); d++) {
             double inst;
             int eff = monitor_tick(d, inst);
             int k = n_util++;
@@ -1021,6 +1031,7 @@ struct WarpSim {
     }
 
     FI void log_event(double t, int kind, long long payload) {
+        if (!G) return;
         int k = n_evlog++;
         if ((G && (P.outputs & GFQ_WANT_EVENTS)) && lane == 0 && k < P.event_log_cap) {
             int64_t o = (int64_t)sid * P.event_log_cap + k;
@@ -1063,7 +1074,7 @@ struct WarpSim {
                 on_arrival(inv);
             } else if (kind == EV_TICK) {
                 tick_on = false;
-                n_ticks++;
+                diag(DG_TICKS);
                 log_event(t, EV_TICK, -1);
                 on_monitor();
             } else {

@@ -52,15 +52,18 @@ for fam, lst in fails.items():
         shown += 1
 print("TOTAL", sum(ok.values()), "/", sum(tot.values()))
 
-# ---- fast build (MQFQ / DeviceSet, no audit logs): dispatch rows, records,
-# exec rows and statistics against the same golden fingerprints
+# ---- fast builds (MQFQ / DeviceSet, no audit logs): dispatch rows, records,
+# exec rows and statistics against the same golden fingerprints.  The
+# single-device subset runs k_sim<false,true>, the full MQFQ set k_sim<false,false>.
 from paper_2507_08954_b200 import _abi  # noqa: E402
 fast = [c for c in cases if c.get("policy", "mqfq") == "mqfq" and not c.get("scripted")]
-outs2, _ = run_cases(fast, eng, outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH,
-                     early_exit=True)
-bad2 = []
-for c, o in zip(fast, outs2):
-    m = compare_to_golden(o, g[c["name"]], exact_keys=("dispatch", "records", "exec"))
-    if m:
-        bad2.append((c["name"], m))
-print("FAST build:", len(fast) - len(bad2), "/", len(fast), bad2[:5])
+one = [c for c in fast if len(c.get("devices", [{}])) == 1]
+for label, sel in (("FAST 1-device build", one), ("FAST multi-device build", fast)):
+    outs2, _ = run_cases(sel, eng, outputs=_abi.WANT_STATS | _abi.WANT_RECORDS |
+                         _abi.WANT_DISPATCH, early_exit=True)
+    bad2 = []
+    for c, o in zip(sel, outs2):
+        m = compare_to_golden(o, g[c["name"]], exact_keys=("dispatch", "records", "exec"))
+        if m:
+            bad2.append((c["name"], m))
+    print(label + ":", len(sel) - len(bad2), "/", len(sel), bad2[:5])

@@ -77,13 +77,15 @@ def test_fast_build_matches_reference(engine):
     match the reference like the generic build's."""
     from gpu_harness import compare_to_golden, run_cases
     from paper_2507_08954_b200 import _abi
-    cases = [c for c in all_cases() if c.get("policy", "mqfq") == "mqfq" and not c.get("scripted")]
-    outs, _ = run_cases(cases, engine, early_exit=True,
-                        outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH)
+    fast = [c for c in all_cases() if c.get("policy", "mqfq") == "mqfq" and not c.get("scripted")]
+    one = [c for c in fast if len(c.get("devices", [{}])) == 1]     # k_sim<false, true>
     gold = golden()
-    bad = {}
-    for c, o in zip(cases, outs):
-        m = compare_to_golden(o, gold[c["name"]], exact_keys=("dispatch", "records", "exec"))
-        if m:
-            bad[c["name"]] = m
-    assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
+    for cases in (one, fast):                                         # ... and <false, false>
+        outs, _ = run_cases(cases, engine, early_exit=True,
+                            outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH)
+        bad = {}
+        for c, o in zip(cases, outs):
+            m = compare_to_golden(o, gold[c["name"]], exact_keys=("dispatch", "records", "exec"))
+            if m:
+                bad[c["name"]] = m
+        assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
