@@ -258,12 +258,15 @@ def run_gfq(args):
     disp_per_step = int(counters[:, 2].sum())
     calls_per_step = int(counters[:, 1].sum())
     events_per_step = int(counters[:, 0].sum())
-    scans = {"gvt_scans": int(counters[:, 5].sum()), "refresh_scans": int(counters[:, 6].sum()),
-             "candidate_scans": int(counters[:, 7].sum()), "ticks": int(counters[:, 8].sum()),
-             "window_memo_hits": int(counters[:, 9].sum()),
-             "window_memo_misses": int(counters[:, 10].sum()),
-             "quiet_drains": int(counters[:, 11].sum()),
-             "max_dynamic_events": int(counters[:, 4].max())}
+    # diagnostic counters exist only in a -DGFQ_DIAG=1 build (zero otherwise)
+    scans = {}
+    if int(counters[:, 8].sum()):
+        scans = {"gvt_scans": int(counters[:, 5].sum()), "refresh_scans": int(counters[:, 6].sum()),
+                 "candidate_scans": int(counters[:, 7].sum()), "ticks": int(counters[:, 8].sum()),
+                 "window_memo_hits": int(counters[:, 9].sum()),
+                 "window_memo_misses": int(counters[:, 10].sum()),
+                 "quiet_drains": int(counters[:, 11].sum()),
+                 "max_dynamic_events": int(counters[:, 4].max())}
 
     # ---- timed region (device time, CUDA events on the launch stream)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

@@ -22,9 +22,9 @@ enum { DV_OUT = 0, DV_EFFD, DV_HROK, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_INSTDIR
        DV_DMAX = DV_NSTATE, DV_POOLMAX, DV_POOLON, DV_DYN,   //  in the 1-device build);
        DV_NI = 16 };                                         //  DeviceConfig copy
 // per-device double fields: state, then a copy of the device's DeviceConfig
-enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_NSTATE,
+enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_OLDT, DD_LKEY, DD_NSTATE,
        DD_MEMCAP = DD_NSTATE, DD_THR, DD_PCIE, DD_BETA, DD_WINDOW, DD_OVERLAP, DD_INVDMAX,
-       DD_ND = 10 };
+       DD_ND = 12 };
 // window-average memo: WDICT distinct utilization values per device,
 // WMEMO direct-mapped (window code, count) -> average entries
 enum { WDICT = 15, WMEMO = 16 };

@@ -51,6 +51,9 @@
 namespace gfq {
 
 #define FULLMASK 0xffffffffu
+#ifndef GFQ_DIAG
+#define GFQ_DIAG 0      // per-warp diagnostic counters (scans, ticks, memo hits, ...)
+#endif
 #define FI __device__ __forceinline__
 typedef unsigned long long u64;
 
@@ -157,7 +160,7 @@ struct WarpSim {
         return ((double*)(sm + P.L.o_dvd))[d * DD_ND + k];
     }
     FI int NDEV() const { return ND1 ? 1 : ndev; }
-    FI void diag(int k, unsigned v = 1) { if (lane == 0) ((uint32_t*)(sm + P.L.o_diag))[k] += v; }
+    FI void diag(int k, unsigned v = 1) { if (GFQ_DIAG && lane == 0) ((uint32_t*)(sm + P.L.o_diag))[k] += v; }
     FI double& UAVG(int d) { return DD(d, DD_UAVG); }
     FI double& SMPT(int d, int i) const { return ((double*)(sm + P.L.o_smp_t))[d * P.L.S + i]; }
     FI double& SMPU(int d, int i) const { return ((double*)(sm + P.L.o_smp_u))[d * P.L.S + i]; }
@@ -231,7 +234,7 @@ struct WarpSim {
         if (kind == EV_TICK) { tick_on = true; tick_t = t; tick_seq = s; return; }
         if (nev >= P.L.E) { fail(GFQ_SIM_EVENT_OVERFLOW); return; }
         int slot = nev++;
-        if (lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
+        if (GFQ_DIAG && lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
         __syncwarp();
         ev_t()[slot] = t; ev_seq()[slot] = s; ev_meta()[slot] = ((uint32_t)kind << 30) | payload;
         __syncwarp();
@@ -590,10 +593,14 @@ struct WarpSim {
         __syncwarp();
         SMPT(d, w) = now; SMPU(d, w) = util;
         __syncwarp();
+        double oldt = ns == 0 ? now : DD(d, DD_OLDT);    // time of the oldest sample
         ns++;
         double horizon = now - DD(d, DD_WINDOW);
         #pragma unroll 1
-        while (ns > 0 && SMPT(d, head) <= horizon) { head++; if (head >= S) head = 0; ns--; }
+        while (ns > 0 && oldt <= horizon) {
+            head++; if (head >= S) head = 0; ns--;
+            oldt = SMPT(d, head);                          // ns >= 1: the new sample stays
+        }
         double avg;
         bool memo = ns <= 14 && zage >= ns;          // key ~0 stays the empty-slot marker
         u64 key = 0; int slot = 0;
@@ -601,7 +608,10 @@ struct WarpSim {
             key = (code & ((1ull << (4 * ns)) - 1)) | ((u64)ns << 60);
             slot = (int)((key * 0x9E3779B97F4A7C15ull) >> 60);
         }
-        if (memo && WKEY(d, slot) == key) {
+        const u64 lkey = (u64)__double_as_longlong(DD(d, DD_LKEY));
+        if (memo && key == lkey) {                    // same window as the last tick
+            avg = UAVG(d);
+        } else if (memo && WKEY(d, slot) == key) {
             avg = WVAL(d, slot);
             diag(DG_WHIT);
         } else {
@@ -624,6 +634,8 @@ struct WarpSim {
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
         DV(d, DV_HROK) = hrok; DV(d, DV_ZAGE) = zage;
         DD(d, DD_WCODE) = __longlong_as_double((long long)code);
+        DD(d, DD_OLDT) = oldt;
+        DD(d, DD_LKEY) = __longlong_as_double((long long)(memo ? key : ~0ull));
         __syncwarp();
         return effd;
     }
@@ -1043,33 +1055,32 @@ struct WarpSim {
     // Simulation.run / step, engine.py:99-119
     FI void run() {
         long long max_events = sim->max_events > 0 ? sim->max_events : 64ll * ((long long)n + 1024);
-        double t_arr = n > 0 ? arr(0) : 0.0;
+        const double INF = __longlong_as_double(0x7ff0000000000000ll);
+        double t_arr = n > 0 ? arr(0) : INF;
         const bool early = P.early_exit && !(G && (P.outputs & GFQ_WANT_EVENTS));
         #pragma unroll 1
         for (;;) {
-            bool has_arr = cursor < n;
             if (!pmin_ok) pool_min();
-            bool has_pool = pmin_slot >= 0;
-            if (!has_arr && !tick_on && !has_pool) break;
-            // exact early exit: only keep-alive rechecks remain, which change
-            // no record, dispatch row, audit row or statistic
-            if (early && !has_arr && !tick_on && tot_pend == 0 && tot_infl == 0) break;
-            int kind; double t; uint32_t sq;
-            if (has_arr) { kind = EV_ARRIVAL; t = t_arr; sq = (uint32_t)cursor; }
-            else { kind = -1; t = 0.0; sq = 0xffffffffu; }
-            if (tick_on && (kind < 0 || tick_t < t || (tick_t == t && tick_seq < sq))) {
-                kind = EV_TICK; t = tick_t; sq = tick_seq;
+            if (!tick_on) {            // no tick scheduled: the run is ending
+                if (cursor >= n && pmin_slot < 0) break;
+                // exact early exit: only keep-alive rechecks remain, which change
+                // no record, dispatch row, audit row or statistic
+                if (early && cursor >= n && tot_pend == 0 && tot_infl == 0) break;
             }
-            if (has_pool && (kind < 0 || pmin_t < t || (pmin_t == t && pmin_seq < sq))) {
-                kind = 4; t = pmin_t; sq = pmin_seq;
-            }
+            // earliest (time, seq): arrivals (seq = trace index < every dynamic
+            // seq) win time ties; absent candidates sit at +inf
+            const double tt = tick_on ? tick_t : INF, tp = pmin_slot >= 0 ? pmin_t : INF;
+            int kind; double t;
+            if (t_arr <= tt && t_arr <= tp && t_arr != INF) { kind = EV_ARRIVAL; t = t_arr; }
+            else if (tick_on && (tt < tp || (tt == tp && tick_seq < pmin_seq))) { kind = EV_TICK; t = tt; }
+            else { kind = 4; t = tp; }
             if (n_events >= max_events) { fail(GFQ_SIM_WATCHDOG); break; }
             now = t;
             n_events++;
             bool dr = true;
             if (kind == EV_ARRIVAL) {
                 int inv = cursor++;
-                if (cursor < n) t_arr = arr(cursor);
+                t_arr = cursor < n ? arr(cursor) : INF;
                 log_event(t, EV_ARRIVAL, inv);
                 on_arrival(inv);
             } else if (kind == EV_TICK) {
