@@ -243,6 +243,12 @@ int  gfq_synchronize(gfq_handle* h);
  * recorded on the launch stream around the sim kernel and the reducer). */
 int  gfq_last_kernel_ms(gfq_handle* h, float* sim_ms, float* reduce_ms);
 
+/* Per-launch kernel times of up to the last GFQ_TIMING_RING launches since
+ * the previous call (oldest first); *n receives the count.  Lets a caller
+ * time the simulation kernel alone over a region of back-to-back launches. */
+#define GFQ_TIMING_RING 256
+int  gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t cap, int32_t* n);
+
 /* Output access. */
 int  gfq_output_info(gfq_handle* h, int32_t id, int64_t* n_elems, int32_t* elem_bytes);
 int  gfq_output_copy(gfq_handle* h, int32_t id, void* host_dst, int64_t bytes);

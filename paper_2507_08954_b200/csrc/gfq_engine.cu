@@ -175,7 +175,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
     w.n = (int)(p.trace_off[t + 1] - w.toff);
     w.nf = p.trace_nf[t];
     w.foff = p.foff + p.foff_off[t];
-    w.tb = p.tab_off[sim->flowtab];
+    w.tb = (int)p.tab_off[sim->flowtab];
     w.roff = p.sim_roff[sid];
     w.policy = sim->policy;
     w.scripted_ = sim->device_model == GFQ_DEVMODEL_SCRIPTED;
@@ -421,6 +421,8 @@ struct gfq_handle {
     int32_t out_b[GFQ_OUT_COUNT_] = {0};
     DBuf comp_lat, comp_meta;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> ring;          // GFQ_TIMING_RING x 3 events
+    int ring_next = 0, ring_count = 0;
     cudaStream_t last_stream = nullptr;
     bool launched = false;
 };
@@ -456,6 +458,8 @@ int gfq_create(int device, gfq_handle** out) {
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     h->smem_optin = (size_t)optin;
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    h->ring.resize(3 * GFQ_TIMING_RING);
+    for (auto& e : h->ring) CK(cudaEventCreate(&e));
     *out = h;
     return GFQ_OK;
 }
@@ -470,6 +474,7 @@ int gfq_destroy(gfq_handle* h) {
     for (DBuf* b : all) b->release();
     for (auto& b : h->out) b.release();
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    for (auto& e : h->ring) if (e) cudaEventDestroy(e);
     delete h;
     return GFQ_OK;
 }
@@ -537,6 +542,7 @@ int gfq_upload_flowtabs(gfq_handle* h, const double* warm_s, const double* cold_
     if (!h || n_tabs < 0 || !off) return set_err(GFQ_EINVAL, "gfq_upload_flowtabs: bad arguments");
     CK(cudaSetDevice(h->device));
     int64_t total = off[n_tabs];
+    if (total >= 0x7fffffff) return set_err(GFQ_EINVAL, "gfq_upload_flowtabs: more than 2^31 flow-table rows");
     for (int64_t i = 0; i < total; i++) {       // FunctionProfile validation, core.py:41-51
         if (!(warm_s[i] > 0)) return set_err(GFQ_EINVAL, "warm_exec_s must be > 0");
         if (!(cold_s[i] >= warm_s[i])) return set_err(GFQ_EINVAL, "cold_exec_s must be >= warm_exec_s");
@@ -827,7 +833,9 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaMemsetAsync(h->work.p, 0, 16, st));
     if (h->cfg.outputs & GFQ_WANT_HIST)
         CK(cudaMemsetAsync(h->out[GFQ_OUT_HIST].p, 0, 8 * h->out_n[GFQ_OUT_HIST], st));
+    cudaEvent_t* re = &h->ring[3 * h->ring_next];
     CK(cudaEventRecord(h->ev[0], st));
+    CK(cudaEventRecord(re[0], st));
     if (h->n_sims > 0) {
         size_t smem = (size_t)h->wpb * h->L.bytes;
         if (h->generic) k_sim<true, false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
@@ -836,12 +844,16 @@ int gfq_launch(gfq_handle* h, void* stream) {
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[1], st));
+    CK(cudaEventRecord(re[1], st));
     if (h->n_sims > 0) {
         int rb = (h->n_sims + h->rwpb - 1) / h->rwpb;
         k_reduce<<<rb, h->rwpb * 32, (size_t)h->rwpb * 60 * h->L.F, st>>>(p);
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[2], st));
+    CK(cudaEventRecord(re[2], st));
+    h->ring_next = (h->ring_next + 1) % GFQ_TIMING_RING;
+    h->ring_count = std::min(h->ring_count + 1, (int)GFQ_TIMING_RING);
     h->last_stream = st;
     h->launched = true;
     return GFQ_OK;
@@ -874,6 +886,25 @@ int gfq_last_kernel_ms(gfq_handle* h, float* sim_ms, float* reduce_ms) {
     CK(cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
     if (sim_ms) *sim_ms = a;
     if (reduce_ms) *reduce_ms = b;
+    return GFQ_OK;
+}
+
+int gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t cap, int32_t* n) {
+    if (!h || cap < 0 || !n) return set_err(GFQ_EINVAL, "gfq_kernel_times: bad arguments");
+    CK(cudaSetDevice(h->device));
+    int cnt = std::min(h->ring_count, (int)cap);
+    int first = (h->ring_next - cnt + GFQ_TIMING_RING) % GFQ_TIMING_RING;
+    for (int i = 0; i < cnt; i++) {
+        cudaEvent_t* re = &h->ring[3 * ((first + i) % GFQ_TIMING_RING)];
+        CK(cudaEventSynchronize(re[2]));
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, re[0], re[1]));
+        CK(cudaEventElapsedTime(&b, re[1], re[2]));
+        if (sim_ms) sim_ms[i] = a;
+        if (reduce_ms) reduce_ms[i] = b;
+    }
+    *n = cnt;
+    h->ring_count = 0;
     return GFQ_OK;
 }
 

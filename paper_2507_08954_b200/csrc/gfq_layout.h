@@ -18,9 +18,10 @@ enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
 
 // per-device int fields
 enum { DV_OUT = 0, DV_EFFD, DV_HROK, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_INSTDIRTY, DV_INSTID,
-       DV_ZAGE, DV_WDICT_N, DV_NSTATE,                       // mutable state (registers
-       DV_DMAX = DV_NSTATE, DV_POOLMAX, DV_POOLON, DV_DYN,   //  in the 1-device build);
-       DV_NI = 16 };                                         //  DeviceConfig copy
+       DV_ZAGE, DV_NSTATE,                                   // hot mutable state (registers
+       DV_WDICT_N = DV_NSTATE,                               //  in the 1-device build);
+       DV_DMAX, DV_POOLMAX, DV_POOLON, DV_DYN,               //  DeviceConfig copy
+       DV_NI = 16 };
 // per-device double fields: state, then a copy of the device's DeviceConfig
 enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_OLDT, DD_LKEY, DD_NSTATE,
        DD_MEMCAP = DD_NSTATE, DD_THR, DD_PCIE, DD_BETA, DD_WINDOW, DD_OVERLAP, DD_INVDMAX,

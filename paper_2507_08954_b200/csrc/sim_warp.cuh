@@ -177,7 +177,8 @@ struct WarpSim {
 
     // ---- per-simulation inputs
     const gfq_sim* sim;
-    int64_t toff, tb, roff;
+    int64_t toff, roff;
+    int tb;
     bool tau_inc;
     const int* foff;
     int n, nf, ndev;
@@ -212,7 +213,7 @@ struct WarpSim {
     bool any_newly;
     bool gmin_ok; u64 gmin;            // (A) cached min okey(vt) over backlogged queues
     double idle_lb;                    // (B) no keep-alive can expire before this
-    long long n_events;
+    int n_events;
     int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog;
     PySum util_sum;
 
@@ -1054,7 +1055,8 @@ struct WarpSim {
 
     // Simulation.run / step, engine.py:99-119
     FI void run() {
-        long long max_events = sim->max_events > 0 ? sim->max_events : 64ll * ((long long)n + 1024);
+        long long me = sim->max_events > 0 ? sim->max_events : 64ll * ((long long)n + 1024);
+        const int max_events = (int)min(me, 0x7fffffffll);
         const double INF = __longlong_as_double(0x7ff0000000000000ll);
         double t_arr = n > 0 ? arr(0) : INF;
         const bool early = P.early_exit && !(G && (P.outputs & GFQ_WANT_EVENTS));

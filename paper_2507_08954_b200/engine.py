@@ -184,6 +184,15 @@ class Engine:
         check(self._L.gfq_last_kernel_ms(self._h, C.byref(a), C.byref(b)))
         return float(a.value) + float(b.value)
 
+    def kernel_times(self, cap: int = 256):
+        """(sim_ms, reduce_ms) arrays of the launches since the last call."""
+        a = np.zeros(cap, dtype=np.float32)
+        b = np.zeros(cap, dtype=np.float32)
+        n = C.c_int32()
+        check(self._L.gfq_kernel_times(self._h, _ptr(a, C.c_float), _ptr(b, C.c_float), cap,
+                                       C.byref(n)))
+        return a[:n.value].astype(np.float64), b[:n.value].astype(np.float64)
+
     def run(self, sims, outputs: int = _abi.WANT_STATS, early_exit: bool = True, **kw):
         self.prepare(sims, outputs, early_exit, **kw)
         self.launch()
