@@ -413,8 +413,8 @@ struct gfq_handle {
     int32_t n_sims = 0;
     gfq_launch_cfg cfg{};
     Layout L{};
-    int wpb = 0, blocks = 0, rwpb = 4;
-    bool generic = true, nd1 = false;
+    int wpb = 0, rwpb = 4;
+    int ccount[3] = {0, 0, 0}, cblocks[3] = {0, 0, 0};   // per kernel class
     bool prepared = false;
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
@@ -674,28 +674,37 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     if ((size_t)L.bytes > h->smem_optin)
         return set_err(GFQ_EINVAL, "gfq_prepare: per-simulation workspace (" + std::to_string(L.bytes) +
                                        " B) exceeds shared memory; reduce flows/pool/event capacity");
-    // the MQFQ-Sticky / DeviceSet build unless a sim or an output needs the
-    // generic one (other policies, scripted devices, audit / event logs)
-    bool generic = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
-    for (int i = 0; i < n_sims && !generic; i++)
-        generic = sims[i].policy != GFQ_POLICY_MQFQ || sims[i].device_model != GFQ_DEVMODEL_DEVICESET;
-    bool nd1 = !generic;
-    for (int i = 0; i < n_sims && nd1; i++) nd1 = sims[i].n_devices == 1;
-    const void* kfn = generic ? (const void*)k_sim<true, false>
-                    : nd1 ? (const void*)k_sim<false, true> : (const void*)k_sim<false, false>;
+    // Kernel classes: the generic build (other policies, scripted devices, audit
+    // or event logs), the MQFQ-Sticky / DeviceSet build, and its 1-device
+    // variant.  Each class runs its own launch over its slice of the work order.
+    const bool logs = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
+    std::vector<int> cls(n_sims);
+    int ccount[3] = {0, 0, 0};
+    for (int i = 0; i < n_sims; i++) {
+        const gfq_sim& s = sims[i];
+        bool fast = !logs && s.policy == GFQ_POLICY_MQFQ && s.device_model == GFQ_DEVMODEL_DEVICESET;
+        cls[i] = !fast ? 0 : (s.n_devices == 1 ? 2 : 1);
+        ccount[cls[i]]++;
+    }
     int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, 4) : 4;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
     size_t smem = (size_t)wpb * L.bytes;
-    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // all of the unified L1/shared array to shared memory: occupancy is bounded
-    // by per-warp simulation state; the kernel's global traffic is tiny
-    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                            (int)cudaSharedmemCarveoutMaxShared));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, wpb * 32, smem));
-    if (per_sm < 1) return set_err(GFQ_EINVAL, "gfq_prepare: kernel does not fit on an SM");
-    int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
-    blocks = std::max(1, std::min(blocks, (n_sims + wpb - 1) / wpb));
+    int cblocks[3] = {0, 0, 0};
+    for (int k = 0; k < 3; k++) {
+        if (!ccount[k]) continue;
+        const void* kfn = k == 0 ? (const void*)k_sim<true, false>
+                        : k == 1 ? (const void*)k_sim<false, false> : (const void*)k_sim<false, true>;
+        CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // all of the unified L1/shared array to shared memory: occupancy is bounded
+        // by per-warp simulation state; the kernel's global traffic is tiny
+        CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, wpb * 32, smem));
+        if (per_sm < 1) return set_err(GFQ_EINVAL, "gfq_prepare: kernel does not fit on an SM");
+        int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
+        cblocks[k] = std::max(1, std::min(blocks, (ccount[k] + wpb - 1) / wpb));
+    }
     int rwpb = 4;
     while (rwpb > 1 && (size_t)rwpb * 60 * L.F > h->smem_optin) rwpb--;
     if ((size_t)rwpb * 60 * L.F > h->smem_optin)
@@ -747,9 +756,11 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
             return set_err(GFQ_EINVAL, "gfq_prepare: sim group out of range");
     }
     // longest-first work order (LPT) for the persistent work queue
+    // per class, longest first (LPT) for the persistent work queues
     std::vector<int32_t> order(n_sims);
     for (int i = 0; i < n_sims; i++) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return cls[a] != cls[b] ? cls[a] < cls[b] : cost[a] > cost[b]; });
     if (n_sims) {
         CK(cudaMemcpy(h->sims.p, sims, sizeof(gfq_sim) * n_sims, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->order.p, order.data(), 4 * n_sims, cudaMemcpyHostToDevice));
@@ -762,10 +773,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->cfg = c;
     h->L = L;
     h->wpb = wpb;
-    h->blocks = blocks;
     h->rwpb = rwpb;
-    h->generic = generic;
-    h->nd1 = nd1;
+    for (int k = 0; k < 3; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; }
     h->prepared = true;
     h->launched = false;
     return GFQ_OK;
@@ -838,9 +847,19 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(re[0], st));
     if (h->n_sims > 0) {
         size_t smem = (size_t)h->wpb * h->L.bytes;
-        if (h->generic) k_sim<true, false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
-        else if (h->nd1) k_sim<false, true><<<h->blocks, h->wpb * 32, smem, st>>>(p);
-        else k_sim<false, false><<<h->blocks, h->wpb * 32, smem, st>>>(p);
+        int off = 0;
+        for (int k = 0; k < 3; k++) {
+            if (!h->ccount[k]) continue;
+            Params pk = p;
+            pk.order = p.order + off;
+            pk.n_sims = h->ccount[k];
+            pk.work = p.work + k;
+            dim3 g(h->cblocks[k]), b(h->wpb * 32);
+            if (k == 0) k_sim<true, false><<<g, b, smem, st>>>(pk);
+            else if (k == 1) k_sim<false, false><<<g, b, smem, st>>>(pk);
+            else k_sim<false, true><<<g, b, smem, st>>>(pk);
+            off += h->ccount[k];
+        }
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[1], st));

@@ -67,3 +67,14 @@ for label, sel in (("FAST 1-device build", one), ("FAST multi-device build", fas
         if m:
             bad2.append((c["name"], m))
     print(label + ":", len(sel) - len(bad2), "/", len(sel), bad2[:5])
+
+# ---- one batch spanning all three kernel classes (no audit logs): generic
+# (other policies, scripted), multi-device MQFQ and 1-device MQFQ launches
+outs3, _ = run_cases(cases, eng, outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH,
+                     early_exit=True)
+bad3 = []
+for c, o in zip(cases, outs3):
+    m = compare_to_golden(o, g[c["name"]], exact_keys=("dispatch", "records", "exec"))
+    if m:
+        bad3.append((c["name"], m))
+print("MIXED-class batch:", len(cases) - len(bad3), "/", len(cases), bad3[:5])

@@ -89,3 +89,18 @@ def test_fast_build_matches_reference(engine):
             if m:
                 bad[c["name"]] = m
         assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
+
+
+def test_mixed_class_batch(engine):
+    """One batch whose sims span the three kernel classes (generic, MQFQ
+    multi-device, MQFQ 1-device): each class runs its own launch over its
+    slice of the work order; every sim must still match the reference."""
+    from gpu_harness import compare_to_golden, run_cases
+    from paper_2507_08954_b200 import _abi
+    cases = all_cases()
+    outs, _ = run_cases(cases, engine, early_exit=True,
+                        outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH)
+    gold = golden()
+    bad = {c["name"]: m for c, o in zip(cases, outs)
+           if (m := compare_to_golden(o, gold[c["name"]], exact_keys=("dispatch", "records", "exec")))}
+    assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
