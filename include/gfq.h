@@ -136,8 +136,12 @@ typedef struct gfq_launch_cfg {
     double   hist_lo_s;         /* log-binned latency histogram range                 */
     double   hist_hi_s;
     int32_t  blocks;            /* 0 = auto (persistent grid)                          */
-    int32_t  reserved;
+    uint32_t flags;             /* GFQ_FLAG_*                                          */
 } gfq_launch_cfg;
+
+/* gfq_launch_cfg.flags */
+#define GFQ_FLAG_FLOWS_GLOBAL 0x1u /* per-flow state in global scratch (automatic when the
+                                      flow count does not fit shared memory)           */
 
 #define GFQ_NCOUNTERS 12
 

@@ -16,6 +16,7 @@ EV_ARRIVAL, EV_COMPLETION, EV_MONITOR_TICK, EV_QUEUE_EXPIRY = 0, 1, 2, 3
 DEVMODEL_DEVICESET, DEVMODEL_SCRIPTED = 0, 1
 MAX_DEVICES = 8
 NCOUNTERS = 12
+FLAG_FLOWS_GLOBAL = 0x1
 
 SIM_STATUS = {
     0: "ok",
@@ -94,7 +95,7 @@ class LaunchCfg(C.Structure):
         ("hist_lo_s", C.c_double),
         ("hist_hi_s", C.c_double),
         ("blocks", C.c_int32),
-        ("reserved", C.c_int32),
+        ("flags", C.c_uint32),
     ]
 
 

@@ -166,8 +166,9 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
 
 
 template <bool G, bool ND1>
-__device__ __forceinline__ void run_one(const Params& p, unsigned char* base, int lane, int sid) {
-    WarpSim<G, ND1> w(p, base, lane, sid);
+__device__ __forceinline__ void run_one(const Params& p, unsigned char* base, unsigned char* fe,
+                                        int lane, int sid) {
+    WarpSim<G, ND1> w(p, base, fe, lane, sid);
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
     const int t = sim->trace;
@@ -195,7 +196,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
             vt[f] = 0.0; lex[f] = 0.0; tau[f] = 0.0; iat[f] = 0.0; larr[f] = 0.0;
             pt[f] = 0; ph[f] = 0; infl[f] = 0; head[f] = -1; done[f] = 0; pend[f] = 0; fst[f] = 0;
         }
-        uint16_t* cnt = (uint16_t*)(base + p.L.o_cnt);
+        uint16_t* cnt = (uint16_t*)(fe + p.L.o_cnt);
         for (int i = lane; i < 3 * w.ndev * p.L.F; i += 32) cnt[i] = 0;
         if (lane < w.ndev) {
             int d = lane;
@@ -283,29 +284,36 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, in
 #ifndef GFQ_MINB
 #define GFQ_MINB 4
 #endif
-template <bool G, bool ND1>
+template <bool G, bool ND1, bool FG>
 __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* base = smem + (size_t)warp * p.L.bytes;
+    unsigned char* slice = smem + (size_t)warp * p.L.bytes;
+    // FG: the flow/event part lives in this warp's global scratch slice
+    unsigned char* fe = FG ? p.gscratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + warp) * p.L.fe_bytes
+                           : slice;
+    unsigned char* base = FG ? slice : slice + p.L.fe_bytes;
     for (;;) {
         int idx = 0;
         if (lane == 0) idx = atomicAdd(p.work, 1);
         idx = __shfl_sync(FULLMASK, idx, 0);
         if (idx >= p.n_sims) break;
-        run_one<G, ND1>(p, base, lane, p.order[idx]);
+        run_one<G, ND1>(p, base, fe, lane, p.order[idx]);
     }
 }
 
 // Result reducer: one warp per finished simulation, over its completion
 // stream (comp_lat / comp_meta, written in completion order by k_sim).
+template <bool FG>
 __global__ void __launch_bounds__(128) k_reduce(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sid = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (sid >= p.n_sims) return;
-    if (p.status[sid] != GFQ_SIM_OK) return;
-    reduce_one(p, smem + (size_t)warp * 60 * p.L.F, lane, sid);
+    const int wpb = blockDim.x >> 5;
+    const size_t scratch = (size_t)60 * p.L.F;
+    unsigned char* base = FG ? p.gscratch + (size_t)(blockIdx.x * wpb + warp) * scratch
+                             : smem + (size_t)warp * scratch;
+    for (int sid = blockIdx.x * wpb + warp; sid < p.n_sims; sid += gridDim.x * wpb)
+        if (p.status[sid] == GFQ_SIM_OK) reduce_one(p, base, lane, sid);
 }
 
 // Trace loader: one warp per trace.  Counting sort of trace positions by
@@ -413,13 +421,14 @@ struct gfq_handle {
     int32_t n_sims = 0;
     gfq_launch_cfg cfg{};
     Layout L{};
-    int wpb = 0, rwpb = 4;
+    int wpb = 0, rwpb = 4, rblocks = 1;
+    bool rglobal = false;
     int ccount[3] = {0, 0, 0}, cblocks[3] = {0, 0, 0};   // per kernel class
     bool prepared = false;
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
     int32_t out_b[GFQ_OUT_COUNT_] = {0};
-    DBuf comp_lat, comp_meta;
+    DBuf comp_lat, comp_meta, gscratch;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ring;          // GFQ_TIMING_RING x 3 events
     int ring_next = 0, ring_count = 0;
@@ -467,7 +476,7 @@ int gfq_create(int device, gfq_handle** out) {
 int gfq_destroy(gfq_handle* h) {
     if (!h) return GFQ_OK;
     cudaSetDevice(h->device);
-    DBuf* all[] = {&h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
+    DBuf* all[] = {&h->gscratch, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
                    &h->fpos, &h->warm, &h->cold, &h->mem, &h->share, &h->weight, &h->hist_row,
                    &h->tab_off, &h->dcfg, &h->execs, &h->sims, &h->order, &h->sim_foff,
                    &h->sim_roff, &h->work, &h->comp_lat, &h->comp_meta};
@@ -670,7 +679,14 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     L.F = (max_nf + 31) & ~31;
     L.ND = nd; L.P = P; L.R = R; L.S = S;
     L.E = c.event_capacity > 0 ? c.event_capacity : std::max(64, ((2 * max_nf + 2 * R * nd + 32) + 31) & ~31);
+    L.flows_global = 0;
     layout_finish(L);
+    // flow counts whose per-simulation state does not fit in shared memory
+    // (or GFQ_FLAG_FLOWS_GLOBAL) put the flow/event part in global scratch
+    if ((c.flags & GFQ_FLAG_FLOWS_GLOBAL) || (size_t)L.bytes > h->smem_optin) {
+        L.flows_global = 1;
+        layout_finish(L);
+    }
     if ((size_t)L.bytes > h->smem_optin)
         return set_err(GFQ_EINVAL, "gfq_prepare: per-simulation workspace (" + std::to_string(L.bytes) +
                                        " B) exceeds shared memory; reduce flows/pool/event capacity");
@@ -682,7 +698,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     int ccount[3] = {0, 0, 0};
     for (int i = 0; i < n_sims; i++) {
         const gfq_sim& s = sims[i];
-        bool fast = !logs && s.policy == GFQ_POLICY_MQFQ && s.device_model == GFQ_DEVMODEL_DEVICESET;
+        bool fast = !logs && !L.flows_global && s.policy == GFQ_POLICY_MQFQ &&
+                    s.device_model == GFQ_DEVMODEL_DEVICESET;
         cls[i] = !fast ? 0 : (s.n_devices == 1 ? 2 : 1);
         ccount[cls[i]]++;
     }
@@ -692,8 +709,9 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     int cblocks[3] = {0, 0, 0};
     for (int k = 0; k < 3; k++) {
         if (!ccount[k]) continue;
-        const void* kfn = k == 0 ? (const void*)k_sim<true, false>
-                        : k == 1 ? (const void*)k_sim<false, false> : (const void*)k_sim<false, true>;
+        const void* kfn = k == 0 ? (L.flows_global ? (const void*)k_sim<true, false, true>
+                                                   : (const void*)k_sim<true, false, false>)
+                        : k == 1 ? (const void*)k_sim<false, false, false> : (const void*)k_sim<false, true, false>;
         CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // all of the unified L1/shared array to shared memory: occupancy is bounded
         // by per-warp simulation state; the kernel's global traffic is tiny
@@ -705,17 +723,25 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
         cblocks[k] = std::max(1, std::min(blocks, (ccount[k] + wpb - 1) / wpb));
     }
+    // reducer: 60 B of scratch per flow per warp, shared memory or global
     int rwpb = 4;
-    while (rwpb > 1 && (size_t)rwpb * 60 * L.F > h->smem_optin) rwpb--;
-    if ((size_t)rwpb * 60 * L.F > h->smem_optin)
-        return set_err(GFQ_EINVAL, "gfq_prepare: too many flows per simulation for the reducer");
-    CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(rwpb * 60 * L.F)));
+    const bool rglobal = L.flows_global || (size_t)60 * L.F > h->smem_optin;
+    if (!rglobal) while (rwpb > 1 && (size_t)rwpb * 60 * L.F > h->smem_optin) rwpb--;
+    int rblocks = std::max(1, std::min((n_sims + rwpb - 1) / rwpb, 8 * h->n_sm));
+    if (!rglobal)
+        CK(cudaFuncSetAttribute(k_reduce<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(rwpb * 60 * L.F)));
+    size_t gscr = 0;
+    if (L.flows_global)
+        for (int k = 0; k < 3; k++) gscr = std::max(gscr, (size_t)cblocks[k] * wpb * L.fe_bytes);
+    if (rglobal) gscr = std::max(gscr, (size_t)rblocks * rwpb * 60 * L.F);
 
     int rc;
     if ((rc = h->sims.ensure(sizeof(gfq_sim) * std::max(n_sims, 1))) || (rc = h->order.ensure(4 * std::max(n_sims, 1))) ||
         (rc = h->sim_foff.ensure(8 * (n_sims + 1))) || (rc = h->sim_roff.ensure(8 * (n_sims + 1))) ||
         (rc = h->work.ensure(16)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
-        (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))))
+        (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))) ||
+        (gscr && (rc = h->gscratch.ensure(gscr))))
         return rc;
     for (int id = 0; id < GFQ_OUT_COUNT_; id++) h->out_n[id] = 0;
     if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, (int64_t)GFQ_NCOUNTERS * n_sims)) ||
@@ -774,6 +800,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->L = L;
     h->wpb = wpb;
     h->rwpb = rwpb;
+    h->rblocks = rblocks;
+    h->rglobal = rglobal;
     for (int k = 0; k < 3; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; }
     h->prepared = true;
     h->launched = false;
@@ -839,6 +867,7 @@ int gfq_launch(gfq_handle* h, void* stream) {
     p.hist_rows = h->cfg.hist_rows; p.hist_bins = h->cfg.hist_bins;
     p.hist_lo = h->cfg.hist_lo_s; p.hist_hi = h->cfg.hist_hi_s;
     p.work = h->work.as<int32_t>();
+    p.gscratch = h->gscratch.as<unsigned char>();
     CK(cudaMemsetAsync(h->work.p, 0, 16, st));
     if (h->cfg.outputs & GFQ_WANT_HIST)
         CK(cudaMemsetAsync(h->out[GFQ_OUT_HIST].p, 0, 8 * h->out_n[GFQ_OUT_HIST], st));
@@ -855,9 +884,11 @@ int gfq_launch(gfq_handle* h, void* stream) {
             pk.n_sims = h->ccount[k];
             pk.work = p.work + k;
             dim3 g(h->cblocks[k]), b(h->wpb * 32);
-            if (k == 0) k_sim<true, false><<<g, b, smem, st>>>(pk);
-            else if (k == 1) k_sim<false, false><<<g, b, smem, st>>>(pk);
-            else k_sim<false, true><<<g, b, smem, st>>>(pk);
+            if (k == 0) {
+                if (h->L.flows_global) k_sim<true, false, true><<<g, b, smem, st>>>(pk);
+                else k_sim<true, false, false><<<g, b, smem, st>>>(pk);
+            } else if (k == 1) k_sim<false, false, false><<<g, b, smem, st>>>(pk);
+            else k_sim<false, true, false><<<g, b, smem, st>>>(pk);
             off += h->ccount[k];
         }
         CK(cudaGetLastError());
@@ -865,8 +896,8 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(h->ev[1], st));
     CK(cudaEventRecord(re[1], st));
     if (h->n_sims > 0) {
-        int rb = (h->n_sims + h->rwpb - 1) / h->rwpb;
-        k_reduce<<<rb, h->rwpb * 32, (size_t)h->rwpb * 60 * h->L.F, st>>>(p);
+        if (h->rglobal) k_reduce<true><<<h->rblocks, h->rwpb * 32, 0, st>>>(p);
+        else k_reduce<false><<<h->rblocks, h->rwpb * 32, (size_t)h->rwpb * 60 * h->L.F, st>>>(p);
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[2], st));

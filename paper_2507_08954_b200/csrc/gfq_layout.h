@@ -42,19 +42,26 @@ struct Layout {
     int32_t P;      // container pool slots per device (pool_max + 1)
     int32_t R;      // running slots per device (max d_max)
     int32_t S;      // utilization-sample ring slots per device
-    // byte offsets inside one warp's slice (all 8-byte aligned)
+    // F-dependent part ("fe"): per-flow state, dynamic events, per-flow
+    // container counts.  Byte offsets from the fe base (8-byte aligned).
     int32_t o_vt, o_lex, o_tau, o_iat, o_larr;          // f64[F]
     int32_t o_pt, o_ph, o_infl, o_head, o_done, o_pend;  // i32[F]
     int32_t o_fst;                                       // u8[F]
     int32_t o_ev_t, o_ev_seq, o_ev_meta;                 // f64[E], u32[E], u32[E]
+    int32_t o_cnt;                                       // u16[ND][3][F]: gpu-warm, host-warm, running
+    int32_t fe_bytes;
+    // device part: offsets from the device base
     int32_t o_dvi, o_dvd;                                // i32[ND][DV_NI], f64[ND][DD_ND]
     int32_t o_smp_t, o_smp_u;                            // f64[ND][S]
     int32_t o_run_i, o_run_d;                            // i32[ND][R][4], f64[ND][R][2]
     int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
-    int32_t o_cnt;                                       // u16[ND][3][F]: gpu-warm, host-warm, running
     int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u64[ND][WMEMO], f64[ND][WMEMO]
     int32_t o_diag;                                      // u32[DG_N]
-    int32_t bytes;                                       // slice size
+    int32_t dev_bytes;
+    // the fe part lives in shared memory in front of the device part, or (for
+    // flow counts whose state does not fit) in a per-warp global scratch slice
+    int32_t flows_global;
+    int32_t bytes;                                       // shared bytes per warp
 };
 
 struct Params {
@@ -97,28 +104,32 @@ struct Params {
     double* event_time; int64_t* event_meta; int64_t* event_count; int64_t event_log_cap;
     unsigned long long* hist; int32_t hist_rows, hist_bins; double hist_lo, hist_hi;
     int32_t* work;                 // work-queue counter
+    unsigned char* gscratch;       // per-warp fe slices when L.flows_global
 };
 
 inline int32_t align8(int32_t x) { return (x + 7) & ~7; }
 
 inline void layout_finish(Layout& L) {
+    const int32_t F = L.F, E = L.E, ND = L.ND, P = L.P, R = L.R, S = L.S;
     int32_t o = 0;
     auto take = [&](int32_t bytes) { int32_t r = o; o = align8(o + bytes); return r; };
-    const int32_t F = L.F, E = L.E, ND = L.ND, P = L.P, R = L.R, S = L.S;
     L.o_vt = take(8 * F); L.o_lex = take(8 * F); L.o_tau = take(8 * F);
     L.o_iat = take(8 * F); L.o_larr = take(8 * F);
     L.o_pt = take(4 * F); L.o_ph = take(4 * F); L.o_infl = take(4 * F);
     L.o_head = take(4 * F); L.o_done = take(4 * F); L.o_pend = take(4 * F);
     L.o_fst = take(F);
     L.o_ev_t = take(8 * E); L.o_ev_seq = take(4 * E); L.o_ev_meta = take(4 * E);
+    L.o_cnt = take(2 * 3 * ND * F);
+    L.fe_bytes = o;
+    o = 0;
     L.o_dvi = take(4 * DV_NI * ND); L.o_dvd = take(8 * DD_ND * ND);
     L.o_smp_t = take(8 * ND * S); L.o_smp_u = take(8 * ND * S);
     L.o_run_i = take(4 * 4 * ND * R); L.o_run_d = take(8 * 2 * ND * R);
     L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);
-    L.o_cnt = take(2 * 3 * ND * F);
     L.o_wdict = take(8 * WDICT * ND); L.o_wkey = take(8 * WMEMO * ND); L.o_wval = take(8 * WMEMO * ND);
     L.o_diag = take(4 * DG_N);
-    L.bytes = o;
+    L.dev_bytes = o;
+    L.bytes = L.flows_global ? L.dev_bytes : L.fe_bytes + L.dev_bytes;
 }
 
 }  // namespace gfq

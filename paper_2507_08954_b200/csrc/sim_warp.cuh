@@ -129,26 +129,27 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 template <bool G, bool ND1>
 struct WarpSim {
     const Params& P;
-    unsigned char* const sm;   // this warp's shared-memory slice
+    unsigned char* const sm;   // device part of this warp's state (shared memory)
+    unsigned char* const fe;   // flow/event part (shared memory, or global scratch)
     const int lane;
     const int sid;
 
     // ---- shared-memory views (offsets live in the kernel's param space)
-    FI double* vt() const { return (double*)(sm + P.L.o_vt); }
-    FI double* lex() const { return (double*)(sm + P.L.o_lex); }
-    FI double* tau() const { return (double*)(sm + P.L.o_tau); }
-    FI double* iat() const { return (double*)(sm + P.L.o_iat); }
-    FI double* larr() const { return (double*)(sm + P.L.o_larr); }
-    FI int* pt() const { return (int*)(sm + P.L.o_pt); }
-    FI int* ph() const { return (int*)(sm + P.L.o_ph); }
-    FI int* infl() const { return (int*)(sm + P.L.o_infl); }
-    FI int* head() const { return (int*)(sm + P.L.o_head); }
-    FI int* done() const { return (int*)(sm + P.L.o_done); }
-    FI int* pend() const { return (int*)(sm + P.L.o_pend); }
-    FI uint8_t* fst() const { return (uint8_t*)(sm + P.L.o_fst); }
-    FI double* ev_t() const { return (double*)(sm + P.L.o_ev_t); }
-    FI uint32_t* ev_seq() const { return (uint32_t*)(sm + P.L.o_ev_seq); }
-    FI uint32_t* ev_meta() const { return (uint32_t*)(sm + P.L.o_ev_meta); }
+    FI double* vt() const { return (double*)(fe + P.L.o_vt); }
+    FI double* lex() const { return (double*)(fe + P.L.o_lex); }
+    FI double* tau() const { return (double*)(fe + P.L.o_tau); }
+    FI double* iat() const { return (double*)(fe + P.L.o_iat); }
+    FI double* larr() const { return (double*)(fe + P.L.o_larr); }
+    FI int* pt() const { return (int*)(fe + P.L.o_pt); }
+    FI int* ph() const { return (int*)(fe + P.L.o_ph); }
+    FI int* infl() const { return (int*)(fe + P.L.o_infl); }
+    FI int* head() const { return (int*)(fe + P.L.o_head); }
+    FI int* done() const { return (int*)(fe + P.L.o_done); }
+    FI int* pend() const { return (int*)(fe + P.L.o_pend); }
+    FI uint8_t* fst() const { return (uint8_t*)(fe + P.L.o_fst); }
+    FI double* ev_t() const { return (double*)(fe + P.L.o_ev_t); }
+    FI uint32_t* ev_seq() const { return (uint32_t*)(fe + P.L.o_ev_seq); }
+    FI uint32_t* ev_meta() const { return (uint32_t*)(fe + P.L.o_ev_meta); }
     // per-device fields; in the 1-device build the mutable ones are registers
     int hv[DV_NSTATE]; double hd[DD_NSTATE];
     FI int& DV(int d, int k) {
@@ -172,7 +173,7 @@ struct WarpSim {
     FI u64& WKEY(int d, int i) const { return ((u64*)(sm + P.L.o_wkey))[d * WMEMO + i]; }
     FI double& WVAL(int d, int i) const { return ((double*)(sm + P.L.o_wval))[d * WMEMO + i]; }
     FI uint16_t& CNT(int d, int kind, int f) const {   // kind: 0 gpu-warm, 1 host-warm, 2 running
-        return ((uint16_t*)(sm + P.L.o_cnt))[(d * 3 + kind) * P.L.F + f];
+        return ((uint16_t*)(fe + P.L.o_cnt))[(d * 3 + kind) * P.L.F + f];
     }
 
     // ---- per-simulation inputs
@@ -217,7 +218,8 @@ struct WarpSim {
     int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog;
     PySum util_sum;
 
-    FI WarpSim(const Params& p, unsigned char* s, int l, int id) : P(p), sm(s), lane(l), sid(id) {}
+    FI WarpSim(const Params& p, unsigned char* s, unsigned char* f, int l, int id)
+        : P(p), sm(s), fe(f), lane(l), sid(id) {}
 
     FI void fail(int st) { if (!status) status = st; }
     FI double ttl(int f) const {                          // FlowQueue.ttl, core.py:140-152

@@ -108,6 +108,43 @@ def c2(seed_base: int = 1, n_seeds: int = 456, duration: float = 600.0,
                               "sims": len(sims)})
 
 
+C4_MEM_MB = [256.0, 512.0, 1024.0, 1500.0, 3000.0]
+
+
+def c4(seed_base: int = 1, n_seeds: int = 4, duration: float = 1800.0, rate: float = 2.0,
+       policies=("mqfq", "fcfs")) -> Workload:
+    """BASELINE C4 (configs[3]): 4096 functions per simulation (Zipf 0.5, ~2.1k
+    touched in 1800 s at 2 rps), heterogeneous memory (mem_mb by rank mod 5),
+    16 GB device, D=4, container pool 32 or 256 -> cold starts, host-warm
+    prefetch and LRU swap all exercised.  Per-flow state exceeds shared
+    memory, so these run the flows-in-global build."""
+    from .core import FunctionProfile
+    n_fn = 4096
+    base = default_profiles(n_fn)
+    profiles = {nm: FunctionProfile(nm, p.warm_exec_s, p.cold_exec_s, C4_MEM_MB[i % 5], 0.38, 1.0)
+                for i, (nm, p) in enumerate(base.items())}
+    order = {nm: i for i, nm in enumerate(profiles)}
+    traces, tabs = [], []
+    seeds = list(range(seed_base, seed_base + n_seeds))
+    for seed in seeds:
+        pt = pack_trace(gen_zipf(n_fn, 0.5, rate, duration, seed).entries, profiles)
+        traces.append(pt)
+        tabs.append(flow_table(pt.names, profiles, None, [order[nm] for nm in pt.names]))
+    dcfgs = [DeviceConfig(d_max=4, pool_max_containers=pm) for pm in (32, 256)]
+    sims = []
+    cfg = SchedulerConfig()
+    for pi, pol in enumerate(policies):
+        for di in range(2):
+            for si in range(n_seeds):
+                sims.append(sim_params(pol, cfg, 1, trace=si, flowtab=si, device_cfg=di,
+                                       group=pi * 2 + di))
+    return Workload("c4", traces, tabs, dcfgs, sims, groups=2 * len(policies), hist_rows=n_fn,
+                    describe={"workload": "C4 large-flow stress: 4096 functions per sim",
+                              "functions": n_fn, "zipf_s": 0.5, "rate_rps": rate,
+                              "duration_s": duration, "mem_mb": C4_MEM_MB, "pool": [32, 256],
+                              "d_max": 4, "policies": list(policies), "sims": len(sims)})
+
+
 def build(name: str, rank: int = 0, **kw) -> Workload:
     """Weak-scaling shard for `rank`: a disjoint block of seeds per GPU."""
     if name == "c3":
@@ -116,6 +153,9 @@ def build(name: str, rank: int = 0, **kw) -> Workload:
     if name == "c2":
         n = kw.get("n_seeds", 456)
         return c2(seed_base=1 + rank * n, n_seeds=n)
+    if name == "c4":
+        n = kw.get("n_seeds", 4)
+        return c4(seed_base=1 + rank * n, n_seeds=n)
     raise ValueError(f"unknown workload {name}")
 
 

@@ -78,3 +78,10 @@ for c, o in zip(cases, outs3):
     if m:
         bad3.append((c["name"], m))
 print("MIXED-class batch:", len(cases) - len(bad3), "/", len(cases), bad3[:5])
+
+
+# ---- flows-in-global build forced on every case (generic, all outputs)
+outs4, _ = run_cases(cases, eng, early_exit=False, event_log_cap=65536, audit_util_cap=16384,
+                     flags=_abi.FLAG_FLOWS_GLOBAL)
+bad4 = [(c["name"], m) for c, o in zip(cases, outs4) if (m := compare_to_golden(o, g[c["name"]]))]
+print("FLOWS-GLOBAL build:", len(cases) - len(bad4), "/", len(cases), bad4[:5])

@@ -104,3 +104,25 @@ def test_mixed_class_batch(engine):
     bad = {c["name"]: m for c, o in zip(cases, outs)
            if (m := compare_to_golden(o, gold[c["name"]], exact_keys=("dispatch", "records", "exec")))}
     assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
+
+
+def test_flows_global_build(engine):
+    """The build that keeps per-flow state in global scratch (used when the
+    flow count does not fit shared memory, e.g. C4's 4096 functions), forced
+    on every golden case with every output."""
+    from gpu_harness import compare_to_golden, run_cases
+    from paper_2507_08954_b200 import _abi
+    cases = all_cases()
+    outs, _ = run_cases(cases, engine, early_exit=False, event_log_cap=65536,
+                        audit_util_cap=16384, flags=_abi.FLAG_FLOWS_GLOBAL)
+    gold = golden()
+    bad = {c["name"]: m for c, o in zip(cases, outs)
+           if (m := compare_to_golden(o, gold[c["name"]]))}
+    assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
+
+
+def test_c4_large_flow_sims_match_oracle(engine):
+    """BASELINE C4: 4096 functions per simulation (2.1k touched), pool 32/256,
+    heterogeneous memory, MQFQ + FCFS: flows-in-global build vs the oracle."""
+    from c4_check import check
+    assert check(1, engine) == []
