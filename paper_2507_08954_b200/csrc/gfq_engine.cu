@@ -247,7 +247,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
     w.tot_pend = 0; w.tot_infl = 0;
     w.fcfs_head = 0; w.fcfs_infl = 0; w.draining = -1;
     w.s_att = 0; w.s_out = 0; w.s_exec = 0;
-    w.status = 0; w.any_newly = false;
+    w.status = 0; w.any_newly = false; w.newly_n = 0;
     w.gmin_ok = false; w.gmin = ~0ull;
     w.idle_lb = __longlong_as_double(0x7ff0000000000000ll);
     w.n_events = 0;

@@ -29,6 +29,8 @@ enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_OLDT, DD_LKEY, DD_NSTATE,
 // window-average memo: WDICT distinct utilization values per device,
 // WMEMO direct-mapped (window code, count) -> average entries
 enum { WDICT = 15, WMEMO = 16 };
+// flows queued for swap-out since the last _swap_out_inactive
+enum { NEWLY_CAP = 32 };
 // per-warp diagnostic counters (shared memory, lane 0 increments)
 enum { DG_MAXEV = 0, DG_GSCAN, DG_RSCAN, DG_CSCAN, DG_TICKS, DG_WHIT, DG_WMISS, DG_QUIET, DG_N };
 
@@ -57,6 +59,7 @@ struct Layout {
     int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
     int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u64[ND][WMEMO], f64[ND][WMEMO]
     int32_t o_diag;                                      // u32[DG_N]
+    int32_t o_newly;                                     // i32[NEWLY_CAP]
     int32_t dev_bytes;
     // the fe part lives in shared memory in front of the device part, or (for
     // flow counts whose state does not fit) in a per-warp global scratch slice
@@ -128,6 +131,7 @@ inline void layout_finish(Layout& L) {
     L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);
     L.o_wdict = take(8 * WDICT * ND); L.o_wkey = take(8 * WMEMO * ND); L.o_wval = take(8 * WMEMO * ND);
     L.o_diag = take(4 * DG_N);
+    L.o_newly = take(4 * NEWLY_CAP);
     L.dev_bytes = o;
     L.bytes = L.flows_global ? L.dev_bytes : L.fe_bytes + L.dev_bytes;
 }

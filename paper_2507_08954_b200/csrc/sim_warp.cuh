@@ -88,17 +88,19 @@ FI double pymin(double a, double b) { return b < a ? b : a; }
 // CPython 3.12 builtin sum() over floats (bltinmodule.c builtin_sum_impl):
 // the first item is added to the int start 0, then Neumaier compensation,
 // the compensation is added once at the end when nonzero and finite.
-struct PySum { double f, c; int n; };
-FI void ps_init(PySum& s) { s.f = 0.0; s.c = 0.0; s.n = 0; }
+//
+// Starting from f = 0.0, c = 0.0, the general step below applied to the first
+// item computes exactly CPython's `0 + x` with a zero compensation term, so
+// no item count or first-item branch is needed (and an empty sum is 0.0).
+struct PySum { double f, c; };
+FI void ps_init(PySum& s) { s.f = 0.0; s.c = 0.0; }
 FI void ps_add(PySum& s, double x) {
-    if (s.n++ == 0) { s.f = 0.0 + x; return; }
     double t = s.f + x;
-    if (fabs(s.f) >= fabs(x)) s.c += (s.f - t) + x;
-    else                      s.c += (x - t) + s.f;
+    double e1 = (s.f - t) + x, e2 = (x - t) + s.f;
+    s.c += fabs(s.f) >= fabs(x) ? e1 : e2;
     s.f = t;
 }
 FI double ps_val(const PySum& s) {
-    if (s.n == 0) return 0.0;
     if (s.c != 0.0 && isfinite(s.c)) return s.f + s.c;
     return s.f;
 }
@@ -172,6 +174,7 @@ struct WarpSim {
     FI double& WDICTV(int d, int i) const { return ((double*)(sm + P.L.o_wdict))[d * WDICT + i]; }
     FI u64& WKEY(int d, int i) const { return ((u64*)(sm + P.L.o_wkey))[d * WMEMO + i]; }
     FI double& WVAL(int d, int i) const { return ((double*)(sm + P.L.o_wval))[d * WMEMO + i]; }
+    FI int* NEWLY() const { return (int*)(sm + P.L.o_newly); }
     FI uint16_t& CNT(int d, int kind, int f) const {   // kind: 0 gpu-warm, 1 host-warm, 2 running
         return ((uint16_t*)(fe + P.L.o_cnt))[(d * 3 + kind) * P.L.F + f];
     }
@@ -212,6 +215,7 @@ struct WarpSim {
     int s_att, s_out, s_exec;
     int status;
     bool any_newly;
+    int newly_n;                       // flows queued for swap-out (list in shared memory)
     bool gmin_ok; u64 gmin;            // (A) cached min okey(vt) over backlogged queues
     double idle_lb;                    // (B) no keep-alive can expire before this
     int n_events;
@@ -222,6 +226,7 @@ struct WarpSim {
         : P(p), sm(s), fe(f), lane(l), sid(id) {}
 
     FI void fail(int st) { if (!status) status = st; }
+#define UNLIKELY(x) __builtin_expect(!!(x), 0)
     FI double ttl(int f) const {                          // FlowQueue.ttl, core.py:140-152
         if (alpha == 0.0) return 0.0;
         if (pt()[f] >= 2) return alpha * iat()[f];       // iat.count = arrivals - 1
@@ -232,10 +237,10 @@ struct WarpSim {
     // event pool (engine.py:83-87: heap of (time, seq, kind, payload))
 
     FI void push(double t, int kind, uint32_t payload) {
-        if (t < now) { fail(GFQ_SIM_PAST_EVENT); return; }     // engine.py:84-85
+        if (UNLIKELY(t < now)) { fail(GFQ_SIM_PAST_EVENT); return; }     // engine.py:84-85
         uint32_t s = seq++;
         if (kind == EV_TICK) { tick_on = true; tick_t = t; tick_seq = s; return; }
-        if (nev >= P.L.E) { fail(GFQ_SIM_EVENT_OVERFLOW); return; }
+        if (UNLIKELY(nev >= P.L.E)) { fail(GFQ_SIM_EVENT_OVERFLOW); return; }
         int slot = nev++;
         if (GFQ_DIAG && lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
         __syncwarp();
@@ -462,7 +467,7 @@ struct WarpSim {
     // ---- running set (Device.running dict, insertion order)
     FI void run_append(int d, int inv, int fn, int st, double duration, double pure) {
         int nr = DV(d, DV_NRUN);
-        if (nr >= P.L.R) { fail(GFQ_SIM_POOL_OVERFLOW); return; }
+        if (UNLIKELY(nr >= P.L.R)) { fail(GFQ_SIM_POOL_OVERFLOW); return; }
         __syncwarp();
         RI(d, nr, 0) = inv; RI(d, nr, 1) = fn; RI(d, nr, 2) = st;
         RD(d, nr, 0) = duration; RD(d, nr, 1) = pure;
@@ -545,7 +550,7 @@ struct WarpSim {
         ust(DV(d, DV_OUT), DV(d, DV_OUT) - 1);
         if (!DV(d, DV_POOLON)) return true;
         int np = DV(d, DV_NP);
-        if (np >= P.L.P) { fail(GFQ_SIM_POOL_OVERFLOW); return false; }
+        if (UNLIKELY(np >= P.L.P)) { fail(GFQ_SIM_POOL_OVERFLOW); return false; }
         // the re-pooled entry is (fn, GPU_WARM, mem[fn], now, evictable=False)
         // whether or not a container was claimed at start (device.py:226-236)
         __syncwarp();
@@ -589,7 +594,7 @@ struct WarpSim {
         inst = util;
         const int S = P.L.S;
         int head = DV(d, DV_SHEAD), ns = DV(d, DV_SN);
-        if (ns >= S) { fail(GFQ_SIM_SAMPLE_OVERFLOW); return DV(d, DV_EFFD); }
+        if (UNLIKELY(ns >= S)) { fail(GFQ_SIM_SAMPLE_OVERFLOW); return DV(d, DV_EFFD); }
         int w = head + ns; if (w >= S) w -= S;
         u64 code = ((u64)__double_as_longlong(DD(d, DD_WCODE)) << 4) | (u64)id;
         int zage = id ? min(DV(d, DV_ZAGE) + 1, 255) : 0;
@@ -681,15 +686,26 @@ struct WarpSim {
         u64 lbk = ~0ull;
         bool newly = false;
         #pragma unroll 1
-        for (int f = lane; f < nf; f += 32) {
-            uint8_t s = fst()[f];
-            if ((s & (FL_CREATED | FL_INACTIVE)) != FL_CREATED) continue;
-            if (pt()[f] - done()[f] != 0) continue;          // backlogged
-            double le = lex()[f], tt = ttl(f);
-            if (now - le >= tt) {
+        for (int base = 0; base < nf; base += 32) {      // warp-uniform trip count
+            const int f = base + lane;
+            bool idle = false, mk = false;
+            uint8_t s = 0;
+            double le = 0.0, tt = 0.0;
+            if (f < nf) {
+                s = fst()[f];
+                idle = (s & (FL_CREATED | FL_INACTIVE)) == FL_CREATED && pt()[f] - done()[f] == 0;
+                if (idle) { le = lex()[f]; tt = ttl(f); mk = now - le >= tt; }
+            }
+            if (!SCRIPTED) {                               // compact the marked flows into the list
+                unsigned bm = __ballot_sync(FULLMASK, mk);
+                int pos = newly_n + __popc(bm & ((1u << lane) - 1));
+                if (mk && pos < NEWLY_CAP) NEWLY()[pos] = f;
+                newly_n += __popc(bm);
+            }
+            if (mk) {
                 fst()[f] = (uint8_t)(s | FL_INACTIVE | (SCRIPTED ? 0 : FL_NEWLY));
                 newly = true;
-            } else {
+            } else if (idle) {
                 u64 k = okey(expiry_lb(le, tt));
                 if (k < lbk) lbk = k;
             }
@@ -890,16 +906,32 @@ struct WarpSim {
             }
         }
         __syncwarp();
-        #pragma unroll 1
-        for (int f = lane; f < nf; f += 32) {
-            uint8_t s = fst()[f];
-            if (s & FL_NEWLY) {
+        if (newly_n <= NEWLY_CAP) {          // the listed flows (usually one)
+            #pragma unroll 1
+            for (int k = 0; k < newly_n; k++) {
+                const int f = NEWLY()[k];
                 #pragma unroll 1
-                for (int d = 0; d < NDEV(); d++) { CNT(d, 1, f) += CNT(d, 0, f); CNT(d, 0, f) = 0; }
-                fst()[f] = (uint8_t)((s & ~FL_NEWLY) | FL_MARKED);
+                for (int d = 0; d < NDEV(); d++) {
+                    uint16_t g = CNT(d, 0, f), hw = CNT(d, 1, f);
+                    __syncwarp();
+                    CNT(d, 1, f) = (uint16_t)(hw + g); CNT(d, 0, f) = 0;
+                    __syncwarp();
+                }
+                ust(fst()[f], (uint8_t)((fst()[f] & ~FL_NEWLY) | FL_MARKED));
             }
+        } else {                             // list overflow: scan every flow
+            #pragma unroll 1
+            for (int f = lane; f < nf; f += 32) {
+                uint8_t s = fst()[f];
+                if (s & FL_NEWLY) {
+                    #pragma unroll 1
+                    for (int d = 0; d < NDEV(); d++) { CNT(d, 1, f) += CNT(d, 0, f); CNT(d, 0, f) = 0; }
+                    fst()[f] = (uint8_t)((s & ~FL_NEWLY) | FL_MARKED);
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
+        newly_n = 0;
     }
 
     // _start, engine.py:187-197
@@ -1032,6 +1064,8 @@ struct WarpSim {
             bool inact = now - le >= tt;
             if (inact && !(s & FL_INACTIVE)) {
                 ust(fst()[fn], (uint8_t)(s | FL_INACTIVE | FL_NEWLY));
+                if (newly_n < NEWLY_CAP) ust(NEWLY()[newly_n], fn);
+                newly_n++;
                 any_newly = true;
             } else if (!inact && (s & FL_INACTIVE)) {
                 // unreachable: INACTIVE is absorbing while idle (lex and ttl
@@ -1078,7 +1112,7 @@ struct WarpSim {
             if (t_arr <= tt && t_arr <= tp && t_arr != INF) { kind = EV_ARRIVAL; t = t_arr; }
             else if (tick_on && (tt < tp || (tt == tp && tick_seq < pmin_seq))) { kind = EV_TICK; t = tt; }
             else { kind = 4; t = tp; }
-            if (n_events >= max_events) { fail(GFQ_SIM_WATCHDOG); break; }
+            if (UNLIKELY(n_events >= max_events)) { fail(GFQ_SIM_WATCHDOG); break; }
             now = t;
             n_events++;
             bool dr = true;
@@ -1107,9 +1141,9 @@ struct WarpSim {
                     dr = false;
                 }
             }
-            if (status) break;
+            if (UNLIKELY(status)) break;
             if (dr) drain();
-            if (status) break;
+            if (UNLIKELY(status)) break;
             if (!SCRIPTED) swap_out_inactive();
         }
     }
