@@ -1122,10 +1122,28 @@ struct WarpSim {
                 log_event(t, EV_ARRIVAL, inv);
                 on_arrival(inv);
             } else if (kind == EV_TICK) {
-                tick_on = false;
-                diag(DG_TICKS);
-                log_event(t, EV_TICK, -1);
-                on_monitor();
+                // A run of ticks: while the drain after a tick is provably quiet
+                // (one counted dispatch() call, no state change) and the next
+                // event is again the tick, stay in this loop.  A tick whose drain
+                // may dispatch falls through to the common drain() below.
+                #pragma unroll 1
+                for (;;) {
+                    tick_on = false;
+                    diag(DG_TICKS);
+                    log_event(now, EV_TICK, -1);
+                    on_monitor();
+                    if (UNLIKELY(status) || !quiet_drain()) break;
+                    n_calls++;
+                    diag(DG_QUIET);
+                    dr = false;
+                    if (!tick_on || UNLIKELY(n_events >= max_events)) break;
+                    if (t_arr <= tick_t) break;                       // an arrival comes first
+                    if (pmin_slot >= 0 && (pmin_t < tick_t || (pmin_t == tick_t && pmin_seq < tick_seq)))
+                        break;                                        // a pooled event comes first
+                    now = tick_t;
+                    n_events++;
+                    dr = true;
+                }
             } else {
                 int slot = pmin_slot;
                 uint32_t meta = ev_meta()[slot];
