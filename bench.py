@@ -226,9 +226,16 @@ def run_gfq(args):
     from paper_2507_08954_b200.engine import Engine
 
     rank, world, local = dist_env()
+    # one process per GPU; GFQ_DIST_BACKEND=gloo and ranks > GPUs (ranks then
+    # share devices) exist only to exercise the multi-rank path on a 1-GPU box
+    backend = os.environ.get("GFQ_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     w = sweep.build(args.workload, rank, **({"n_seeds": args.seeds} if args.seeds else {}))
     eng = Engine(local)
     w.upload(eng)
@@ -247,7 +254,12 @@ def run_gfq(args):
     def step():
         eng.launch(stream)
         if hist_t is not None:
-            dist.all_reduce(hist_t)       # histogram gather over NVLink (NCCL)
+            if backend == "nccl":
+                dist.all_reduce(hist_t)   # histogram gather over NVLink (NCCL)
+            else:
+                h = hist_t.cpu()
+                dist.all_reduce(h)
+                hist_t.copy_(h)
 
     for _ in range(max(args.warmup, 0)):
         flush.fill_(1)
@@ -289,7 +301,7 @@ def run_gfq(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(sum(step_ms))
     t = torch.tensor([tot_ms, float(disp_per_step * args.steps)], dtype=torch.float64,
-                     device="cuda")
+                     device="cuda" if backend == "nccl" else "cpu")
     if world > 1:
         tm = t[:1].clone(); dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         td = t[1:].clone(); dist.all_reduce(td)
@@ -408,7 +420,8 @@ def e2e_run(eng, w, outputs, kw, steps, world, dist):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     if dist:
-        t = torch.tensor([dt, float(disp)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt, float(disp)], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
         tm = t[:1].clone(); dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         td = t[1:].clone(); dist.all_reduce(td)
         dt, disp = float(tm.item()), float(td.item())
