@@ -165,10 +165,11 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
 }
 
 
-template <bool G, bool ND1>
+template <int POL, bool ND1>
 __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, unsigned char* fe,
                                         int lane, int sid) {
-    WarpSim<G, ND1> w(p, base, fe, lane, sid);
+    constexpr bool G = POL == PB_GENERIC;
+    WarpSim<POL, ND1> w(p, base, fe, lane, sid);
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
     const int t = sim->trace;
@@ -284,7 +285,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
 #ifndef GFQ_MINB
 #define GFQ_MINB 4
 #endif
-template <bool G, bool ND1, bool FG>
+template <int POL, bool ND1, bool FG>
 __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ P
         if (lane == 0) idx = atomicAdd(p.work, 1);
         idx = __shfl_sync(FULLMASK, idx, 0);
         if (idx >= p.n_sims) break;
-        run_one<G, ND1>(p, base, fe, lane, p.order[idx]);
+        run_one<POL, ND1>(p, base, fe, lane, p.order[idx]);
     }
 }
 
@@ -364,6 +365,21 @@ __global__ void k_trace_index(const int32_t* flow, const int64_t* trace_off, con
 
 using namespace gfq;
 
+// the k_sim instantiation of each kernel class (see gfq_prepare)
+enum { NCLASS = 6 };
+static const void* class_kernel(int k, bool flows_global) {
+    switch (k) {
+        case 1: return (const void*)k_sim<PB_MQFQ, false, false>;
+        case 2: return (const void*)k_sim<PB_MQFQ, true, false>;
+        case 3: return (const void*)k_sim<PB_FCFS, true, false>;
+        case 4: return (const void*)k_sim<PB_BATCH, true, false>;
+        case 5: return (const void*)k_sim<PB_SJF, true, false>;
+        default: return flows_global ? (const void*)k_sim<PB_GENERIC, false, true>
+                                     : (const void*)k_sim<PB_GENERIC, false, false>;
+    }
+}
+
+
 namespace {
 
 thread_local std::string g_err;
@@ -423,7 +439,7 @@ struct gfq_handle {
     Layout L{};
     int wpb = 0, rwpb = 4, rblocks = 1;
     bool rglobal = false;
-    int ccount[3] = {0, 0, 0}, cblocks[3] = {0, 0, 0};   // per kernel class
+    int ccount[NCLASS] = {0}, cblocks[NCLASS] = {0};   // per kernel class
     bool prepared = false;
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
@@ -690,28 +706,35 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     if ((size_t)L.bytes > h->smem_optin)
         return set_err(GFQ_EINVAL, "gfq_prepare: per-simulation workspace (" + std::to_string(L.bytes) +
                                        " B) exceeds shared memory; reduce flows/pool/event capacity");
-    // Kernel classes: the generic build (other policies, scripted devices, audit
-    // or event logs), the MQFQ-Sticky / DeviceSet build, and its 1-device
-    // variant.  Each class runs its own launch over its slice of the work order.
+    // Kernel classes (one launch each over its slice of the work order):
+    //   0 generic (any policy, scripted devices, audit / event logs, large F)
+    //   1 MQFQ-Sticky on a multi-device DeviceSet
+    //   2..5 one policy (MQFQ / FCFS / Batch / SJF) on a 1-device DeviceSet
     const bool logs = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
     std::vector<int> cls(n_sims);
-    int ccount[3] = {0, 0, 0};
+    int ccount[NCLASS] = {0};
     for (int i = 0; i < n_sims; i++) {
         const gfq_sim& s = sims[i];
-        bool fast = !logs && !L.flows_global && s.policy == GFQ_POLICY_MQFQ &&
-                    s.device_model == GFQ_DEVMODEL_DEVICESET;
-        cls[i] = !fast ? 0 : (s.n_devices == 1 ? 2 : 1);
-        ccount[cls[i]]++;
+        int k = 0;
+        if (!logs && !L.flows_global && s.device_model == GFQ_DEVMODEL_DEVICESET) {
+            if (s.n_devices == 1) {
+                k = s.policy == GFQ_POLICY_MQFQ ? 2
+                  : (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) ? 3
+                  : s.policy == GFQ_POLICY_BATCH ? 4 : 5;
+            } else if (s.policy == GFQ_POLICY_MQFQ) {
+                k = 1;
+            }
+        }
+        cls[i] = k;
+        ccount[k]++;
     }
     int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, 4) : 4;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
     size_t smem = (size_t)wpb * L.bytes;
-    int cblocks[3] = {0, 0, 0};
-    for (int k = 0; k < 3; k++) {
+    int cblocks[NCLASS] = {0};
+    for (int k = 0; k < NCLASS; k++) {
         if (!ccount[k]) continue;
-        const void* kfn = k == 0 ? (L.flows_global ? (const void*)k_sim<true, false, true>
-                                                   : (const void*)k_sim<true, false, false>)
-                        : k == 1 ? (const void*)k_sim<false, false, false> : (const void*)k_sim<false, true, false>;
+        const void* kfn = class_kernel(k, L.flows_global);
         CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // all of the unified L1/shared array to shared memory: occupancy is bounded
         // by per-warp simulation state; the kernel's global traffic is tiny
@@ -733,7 +756,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
                                 (int)(rwpb * 60 * L.F)));
     size_t gscr = 0;
     if (L.flows_global)
-        for (int k = 0; k < 3; k++) gscr = std::max(gscr, (size_t)cblocks[k] * wpb * L.fe_bytes);
+        for (int k = 0; k < NCLASS; k++) gscr = std::max(gscr, (size_t)cblocks[k] * wpb * L.fe_bytes);
     if (rglobal) gscr = std::max(gscr, (size_t)rblocks * rwpb * 60 * L.F);
 
     int rc;
@@ -802,7 +825,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->rwpb = rwpb;
     h->rblocks = rblocks;
     h->rglobal = rglobal;
-    for (int k = 0; k < 3; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; }
+    for (int k = 0; k < NCLASS; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; }
     h->prepared = true;
     h->launched = false;
     return GFQ_OK;
@@ -877,18 +900,15 @@ int gfq_launch(gfq_handle* h, void* stream) {
     if (h->n_sims > 0) {
         size_t smem = (size_t)h->wpb * h->L.bytes;
         int off = 0;
-        for (int k = 0; k < 3; k++) {
+        for (int k = 0; k < NCLASS; k++) {
             if (!h->ccount[k]) continue;
             Params pk = p;
             pk.order = p.order + off;
             pk.n_sims = h->ccount[k];
             pk.work = p.work + k;
             dim3 g(h->cblocks[k]), b(h->wpb * 32);
-            if (k == 0) {
-                if (h->L.flows_global) k_sim<true, false, true><<<g, b, smem, st>>>(pk);
-                else k_sim<true, false, false><<<g, b, smem, st>>>(pk);
-            } else if (k == 1) k_sim<false, false, false><<<g, b, smem, st>>>(pk);
-            else k_sim<false, true, false><<<g, b, smem, st>>>(pk);
+            void* args[] = {&pk};
+            CK(cudaLaunchKernel(class_kernel(k, h->L.flows_global), g, b, args, smem, st));
             off += h->ccount[k];
         }
         CK(cudaGetLastError());

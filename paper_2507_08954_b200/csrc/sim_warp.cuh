@@ -128,8 +128,13 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 // ------------------------------------------------------------------------
 // the per-warp simulation
 
-template <bool G, bool ND1>
+// Build classes: PB_GENERIC handles every policy, the scripted token provider
+// and the audit / event logs; the others are one policy on a DeviceSet.
+enum { PB_GENERIC = 0, PB_MQFQ = 1, PB_FCFS = 2, PB_BATCH = 3, PB_SJF = 4 };
+
+template <int POL, bool ND1>
 struct WarpSim {
+    static constexpr bool G = POL == PB_GENERIC;
     const Params& P;
     unsigned char* const sm;   // device part of this warp's state (shared memory)
     unsigned char* const fe;   // flow/event part (shared memory, or global scratch)
@@ -191,8 +196,10 @@ struct WarpSim {
     // G = generic build (every policy, the scripted token provider, audit and
     // event logs); !G = the MQFQ-Sticky / DeviceSet build the sweeps run
 #define SCRIPTED (G && scripted_)
-#define MQFQ (!G || mqfq_)
-#define FCFS (G && fcfs_)
+#define MQFQ (G ? mqfq_ : POL == PB_MQFQ)
+#define FCFS (G ? fcfs_ : POL == PB_FCFS)
+#define BATCH (G ? policy == GFQ_POLICY_BATCH : POL == PB_BATCH)
+#define SJF (G ? policy == GFQ_POLICY_SJF : POL == PB_SJF)
     double T, alpha, dttl, period;
 
     FI double arr(int i) const { return P.arrival[toff + i]; }
@@ -782,8 +789,8 @@ struct WarpSim {
             if (tot_pend > 0 && !certain_refusal()) fn = mqfq_candidate();
         } else if (tot_pend > 0 && !certain_refusal()) {
             if (FCFS) fn = fcfs_head < cursor ? flw(fcfs_head) : -1;   // policies.py:129-139
-            else if (G && policy == GFQ_POLICY_BATCH) fn = batch_candidate();
-            else if (G) fn = sjf_candidate();
+            else if (BATCH) fn = batch_candidate();
+            else if (SJF) fn = sjf_candidate();
         }
         if (fn < 0) return -1;
         int st = 0;
@@ -807,7 +814,7 @@ struct WarpSim {
             ph()[fn] = k; head()[fn] = nxt; pend()[fn] = pe; infl()[fn] = ninf;
             if (MQFQ) { vt()[fn] = nvt; lex()[fn] = now; }
             __syncwarp();
-            if ((G && policy == GFQ_POLICY_BATCH)) draining = fn;
+            if (BATCH) draining = fn;
             if (MQFQ) {
                 if (gmin_ok && nvt != vt_before && okey(vt_before) == gmin) gmin_ok = false;
                 audit_dispatch(inv, vt_before, gvt, pe + 1, ninf);
@@ -1170,4 +1177,6 @@ struct WarpSim {
 #undef SCRIPTED
 #undef MQFQ
 #undef FCFS
+#undef BATCH
+#undef SJF
 }  // namespace gfq
