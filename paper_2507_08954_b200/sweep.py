@@ -145,6 +145,58 @@ def c4(seed_base: int = 1, n_seeds: int = 4, duration: float = 1800.0, rate: flo
                               "d_max": 4, "policies": list(policies), "sims": len(sims)})
 
 
+C5_T = [0.0, 2.0, 10.0, 50.0]
+C5_ALPHA = [0.0, 1.0, 2.0, 8.0]
+C5_D = [1, 2, 3, 4]
+C5_MEM_MB = [256.0, 512.0, 1024.0, 1500.0, 3000.0, 6000.0]
+C5_SHARE = [0.2, 0.38, 0.5]
+C5_RHO = [0.7, 0.9, 1.0, 1.1]
+
+
+def c5(seed_base: int = 1, n_traces: int = 1563, duration: float = 600.0) -> Workload:
+    """BASELINE C5 (configs[4]) per GPU: the 1M-simulation sensitivity sweep
+    is 8 x ~125k.  Every trace (F=100 functions, heterogeneous memory /
+    compute share / weight by rank, load rho in {0.7,0.9,1.0,1.1}) runs 80
+    configurations: MQFQ-Sticky over T x alpha x D (64) and FCFS / Batch / SJF /
+    fcfs_naive over D (16)."""
+    from .core import FunctionProfile
+    n_fn = 100
+    base = default_profiles(n_fn)
+    profiles = {nm: FunctionProfile(nm, p.warm_exec_s, p.cold_exec_s, C5_MEM_MB[i % 6],
+                                    C5_SHARE[i % 3], 2.0 if i % 7 == 0 else 1.0)
+                for i, (nm, p) in enumerate(base.items())}
+    order = {nm: i for i, nm in enumerate(profiles)}
+    shares = [(k + 1) ** -1.5 for k in range(n_fn)]
+    tot = sum(shares)
+    mean_exec = sum(sh / tot * p.warm_exec_s for sh, p in zip(shares, profiles.values()))
+    traces, tabs = [], []
+    for j in range(n_traces):
+        rate = C5_RHO[j % 4] * 1.8 / mean_exec
+        pt = pack_trace(gen_zipf(n_fn, 1.5, rate, duration, seed_base + j).entries, profiles)
+        traces.append(pt)
+        tabs.append(flow_table(pt.names, profiles, None, [order[nm] for nm in pt.names]))
+    dcfgs = [DeviceConfig(d_max=d) for d in C5_D] + \
+            [DeviceConfig(d_max=d, pool_enabled=False) for d in C5_D]
+    sims = []
+    for ti in range(n_traces):
+        for t in C5_T:
+            for a in C5_ALPHA:
+                for di in range(4):
+                    sims.append(sim_params("mqfq", SchedulerConfig(t_overrun=t, alpha=a), 1,
+                                           trace=ti, flowtab=ti, device_cfg=di, group=0))
+        for gi, pol in enumerate(("fcfs", "batch", "sjf", "fcfs_naive")):
+            for di in range(4):
+                sims.append(sim_params(pol, SchedulerConfig(), 1, trace=ti, flowtab=ti,
+                                       device_cfg=di + (4 if pol == "fcfs_naive" else 0),
+                                       group=1 + gi))
+    return Workload("c5", traces, tabs, dcfgs, sims, groups=5, hist_rows=n_fn,
+                    describe={"workload": "C5 sensitivity sweep, per-GPU shard of 1M sims",
+                              "functions": n_fn, "traces": n_traces, "rho": C5_RHO,
+                              "policies": ["mqfq", "fcfs", "batch", "sjf", "fcfs_naive"],
+                              "mem_mb": C5_MEM_MB, "compute_share": C5_SHARE,
+                              "duration_s": duration, "sims": len(sims)})
+
+
 def build(name: str, rank: int = 0, **kw) -> Workload:
     """Weak-scaling shard for `rank`: a disjoint block of seeds per GPU."""
     if name == "c3":
@@ -156,6 +208,9 @@ def build(name: str, rank: int = 0, **kw) -> Workload:
     if name == "c4":
         n = kw.get("n_seeds", 4)
         return c4(seed_base=1 + rank * n, n_seeds=n)
+    if name == "c5":
+        n = kw.get("n_seeds", 1563)
+        return c5(seed_base=1 + rank * n, n_traces=n)
     raise ValueError(f"unknown workload {name}")
 
 
