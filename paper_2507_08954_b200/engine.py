@@ -412,6 +412,110 @@ def run_simulation(trace, profiles, policy, devices, tau_includes_overheads: boo
     return out
 
 
+# event kinds, engine.py:20-23
+ARRIVAL, COMPLETION, MONITOR_TICK, QUEUE_EXPIRY = 0, 1, 2, 3
+
+
+class Simulation:
+    """Drop-in for ``gpufairq.engine.Simulation`` (engine.py:46-119).
+
+    Construction validates like the reference (unknown functions and
+    decreasing arrival times raise ``ValueError``).  On first ``step()`` or
+    ``run()`` the whole simulation runs on the GPU in parity mode (processed-
+    event log, records, dispatch rows, audit); ``step()`` then replays the
+    processed events in order as the reference's ``(time, kind, payload)``
+    tuples -- an ``Invocation`` for arrivals, its ``uid`` for completions,
+    ``None`` for monitor ticks, the function name for keep-alive expiries --
+    advancing ``now`` and appending each completion's ``InvocationRecord``.
+    """
+
+    def __init__(self, trace, profiles, policy, devices, tau_includes_overheads: bool = False,
+                 *, device: int = 0):
+        from .core import Invocation
+        self._pt = pack_trace(trace.entries, profiles)
+        self.trace, self.profiles, self.policy, self.devices = trace, profiles, policy, devices
+        self.tau_includes_overheads = tau_includes_overheads
+        self._device = device
+        self.now = 0.0
+        self.records: list = []
+        self.audit = AuditLog()
+        self._inv = [Invocation(function=nm, arrival_s=t) for t, nm in trace.entries]
+        self._events = None
+        self._pos = 0
+        self._result = None
+
+    def _ensure(self) -> None:
+        if self._events is not None:
+            return
+        pt = self._pt
+        cfg = self.policy.cfg
+        eng = default_engine(self._device)
+        dcfgs = _device_cfgs(self.devices)
+        eng.upload_traces([pt])
+        eng.upload_flowtabs([flow_table(pt.names, self.profiles, getattr(cfg, "weights", None))])
+        eng.upload_device_cfgs(dcfgs)
+        sim = sim_params(self.policy.kind, cfg, len(dcfgs),
+                         tau_includes_overheads=self.tau_includes_overheads)
+        cap = 64 * (pt.n + 1024)
+        res = eng.run([sim], outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
+                      _abi.WANT_AUDIT | _abi.WANT_EVENTS, early_exit=False, event_log_cap=cap,
+                      audit_util_cap=cap, audit_backlog_cap=2 * pt.n + 2)
+        self._result = to_sim_result(res, 0, pt)
+        rec = res.records(0)
+        for p, inv in enumerate(self._inv):
+            inv.dispatch_s = float(rec["dispatch"][p])
+            inv.complete_s = float(rec["complete"][p])
+            inv.start_state = STATE_BY_CODE[int(rec["state"][p])]
+        self._rec_of = {}
+        order = rec["order"]
+        for p in range(pt.n):
+            self._rec_of[p] = self._result.records[int(order[p])]
+        et, em = res.event_rows(0)
+        evs = []
+        for t, m in zip(et.tolist(), em.tolist()):
+            kind, pay = m & 3, m >> 2
+            if kind == ARRIVAL:
+                evs.append((t, kind, self._inv[pay]))
+            elif kind == COMPLETION:
+                evs.append((t, kind, self._inv[pay].uid, pay))
+            elif kind == MONITOR_TICK:
+                evs.append((t, kind, None))
+            else:
+                evs.append((t, kind, pt.names[pay]))
+        self._events = evs
+
+    def step(self):
+        """Process the earliest event; returns (time, kind, payload) or None."""
+        self._ensure()
+        if self._pos >= len(self._events):
+            return None
+        ev = self._events[self._pos]
+        self._pos += 1
+        self.now = ev[0]
+        if ev[1] == COMPLETION:
+            self.records.append(self._rec_of[ev[3]])
+            ev = ev[:3]
+        if self._pos == len(self._events):
+            self._finish()
+        return ev
+
+    def _finish(self) -> None:
+        a = self._result.audit
+        self.audit.backlog, self.audit.util, self.audit.exec = a.backlog, a.util, a.exec
+        self.audit.dispatches = a.dispatches
+        log = getattr(self.policy, "dispatch_log", None)
+        if isinstance(log, list) and not log:
+            log.extend(a.dispatches)
+
+    def run(self) -> SimResult:
+        while self.step() is not None:
+            pass
+        self._ensure()
+        if not self._events:
+            self._finish()
+        return SimResult(records=self.records, audit=self.audit)
+
+
 def to_sim_result(res: BatchResult, i: int, pt: PackedTrace) -> SimResult:
     names = pt.names
     rec = res.records(i)
@@ -446,5 +550,5 @@ def to_sim_result(res: BatchResult, i: int, pt: PackedTrace) -> SimResult:
     return SimResult(records=records, audit=audit)
 
 
-__all__ = ["Engine", "BatchResult", "run_simulation", "sim_params", "SimResult",
+__all__ = ["Engine", "BatchResult", "Simulation", "run_simulation", "sim_params", "SimResult",
            "InvocationRecord", "AuditLog", "FlowTable", "PackedTrace", "default_engine"]
