@@ -184,6 +184,12 @@ enum gfq_output_id {
     GFQ_OUT_EVENT_META,        /* int64  [sims][event_log_cap]: payload<<2 | kind */
     GFQ_OUT_EVENT_COUNT,       /* int64  [sims]                                   */
     GFQ_OUT_HIST,              /* uint64 [groups][rows][bins]                     */
+    GFQ_OUT_FAIR_ROWS,         /* double [windows][5]: w0, service_sum, max_gap,
+                                  bound, bound_conservative  (gfq_fairness)      */
+    GFQ_OUT_FAIR_META,         /* int64  [windows][6]: comparable, n_qualified,
+                                  qualified-set hash, hi flow, lo flow, violated */
+    GFQ_OUT_FAIR_OFF,          /* int64  [sims+1] window-row offset of each sim  */
+    GFQ_OUT_FAIR_COUNT,        /* int64  [sims][3]: windows, comparable, violated */
     GFQ_OUT_COUNT_
 };
 
@@ -257,6 +263,15 @@ int  gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t ca
 int  gfq_output_info(gfq_handle* h, int32_t id, int64_t* n_elems, int32_t* elem_bytes);
 int  gfq_output_copy(gfq_handle* h, int32_t id, void* host_dst, int64_t bytes);
 int  gfq_output_device_ptr(gfq_handle* h, int32_t id, void** dptr);
+
+/* Fairness audit of the last (synchronized) batch: metrics.service_gap_report
+ * (metrics.py:106-187) per simulation, on the GPU.  Needs a batch run with
+ * GFQ_WANT_RECORDS | GFQ_WANT_AUDIT.  d_max[n_sims] is each sim's
+ * SchedulerConfig.d_max (the reference's fallback D); report_weight holds
+ * cfg.weights.get(f, 1.0) for every uploaded flow-table row (same offsets).
+ * Window rows land in GFQ_OUT_FAIR_*; the call synchronizes. */
+int  gfq_fairness(gfq_handle* h, double window_s, const int32_t* d_max,
+                  const double* report_weight, int64_t n_weights);
 
 /* Convenience: prepare + launch + synchronize on the default stream.
  * The drop-in for run_simulation over a batch (engine.py:214-218). */

@@ -38,7 +38,8 @@ WANT_STATS, WANT_RECORDS, WANT_DISPATCH, WANT_AUDIT, WANT_EVENTS, WANT_HIST = (
  OUT_DSP_INV, OUT_DSP_VT_BEFORE, OUT_DSP_GVT, OUT_DSP_QLEN, OUT_DSP_INFLIGHT,
  OUT_UTIL_ROWS, OUT_UTIL_META, OUT_BACKLOG_TIME, OUT_BACKLOG_META,
  OUT_BACKLOG_COUNT, OUT_EVENT_TIME, OUT_EVENT_META, OUT_EVENT_COUNT,
- OUT_HIST, OUT_COUNT_) = range(29)
+ OUT_HIST, OUT_FAIR_ROWS, OUT_FAIR_META, OUT_FAIR_OFF, OUT_FAIR_COUNT,
+ OUT_COUNT_) = range(33)
 
 
 class DeviceCfg(C.Structure):

@@ -42,6 +42,7 @@ _SIGS = {
     "gfq_output_info": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_int64), _P(C.c_int32)]),
     "gfq_output_copy": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
     "gfq_output_device_ptr": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_void_p)]),
+    "gfq_fairness": (C.c_int, [C.c_void_p, C.c_double, _P(C.c_int32), _P(C.c_double), C.c_int64]),
     "gfq_run": (C.c_int, [C.c_void_p, _P(_abi.Sim), C.c_int32, _P(_abi.LaunchCfg)]),
 }
 EXPORTS = tuple(_SIGS)

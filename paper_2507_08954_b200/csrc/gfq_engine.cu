@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "sim_warp.cuh"
+#include "fairness.cuh"
 
 namespace gfq {
 
@@ -444,7 +445,7 @@ struct gfq_handle {
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
     int32_t out_b[GFQ_OUT_COUNT_] = {0};
-    DBuf comp_lat, comp_meta, gscratch;
+    DBuf comp_lat, comp_meta, comp_pos, gscratch, fscratch;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ring;          // GFQ_TIMING_RING x 3 events
     int ring_next = 0, ring_count = 0;
@@ -458,7 +459,8 @@ static const int32_t kOutBytes[GFQ_OUT_COUNT_] = {
     4, 8, 8, 4, 4,            // dsp inv vt gvt qlen infl
     8, 4, 8, 4, 8,            // util rows/meta, backlog time/meta/count
     8, 8, 8,                  // event time/meta/count
-    8};                       // hist
+    8,                        // hist
+    8, 8, 8, 8};              // fairness rows/meta/offsets/counts
 
 extern "C" {
 
@@ -492,7 +494,7 @@ int gfq_create(int device, gfq_handle** out) {
 int gfq_destroy(gfq_handle* h) {
     if (!h) return GFQ_OK;
     cudaSetDevice(h->device);
-    DBuf* all[] = {&h->gscratch, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
+    DBuf* all[] = {&h->gscratch, &h->fscratch, &h->comp_pos, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
                    &h->fpos, &h->warm, &h->cold, &h->mem, &h->share, &h->weight, &h->hist_row,
                    &h->tab_off, &h->dcfg, &h->execs, &h->sims, &h->order, &h->sim_foff,
                    &h->sim_roff, &h->work, &h->comp_lat, &h->comp_meta};
@@ -764,7 +766,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         (rc = h->sim_foff.ensure(8 * (n_sims + 1))) || (rc = h->sim_roff.ensure(8 * (n_sims + 1))) ||
         (rc = h->work.ensure(16)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
         (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))) ||
-        (gscr && (rc = h->gscratch.ensure(gscr))))
+        (gscr && (rc = h->gscratch.ensure(gscr))) ||
+        ((c.outputs & GFQ_WANT_RECORDS) && (rc = h->comp_pos.ensure(4 * std::max<int64_t>(recs, 1)))))
         return rc;
     for (int id = 0; id < GFQ_OUT_COUNT_; id++) h->out_n[id] = 0;
     if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, (int64_t)GFQ_NCOUNTERS * n_sims)) ||
@@ -838,10 +841,7 @@ int gfq_sim_offsets(gfq_handle* h, int64_t* flow_off, int64_t* rec_off) {
     return GFQ_OK;
 }
 
-int gfq_launch(gfq_handle* h, void* stream) {
-    if (!h || !h->prepared) return set_err(GFQ_EINVAL, "gfq_launch: no staged batch");
-    CK(cudaSetDevice(h->device));
-    cudaStream_t st = (cudaStream_t)stream;
+static Params make_params(gfq_handle* h) {
     Params p{};
     p.sims = h->sims.as<gfq_sim>(); p.order = h->order.as<int32_t>(); p.n_sims = h->n_sims;
     p.arrival = h->arrival.as<double>(); p.flow = h->flow.as<int32_t>();
@@ -864,6 +864,7 @@ int gfq_launch(gfq_handle* h, void* stream) {
     p.f_var = h->out[GFQ_OUT_FLOW_VAR].as<double>();
     p.f_cold = h->out[GFQ_OUT_FLOW_COLD_PCT].as<double>();
     p.comp_lat = h->comp_lat.as<double>(); p.comp_meta = h->comp_meta.as<int32_t>();
+    p.comp_pos = h->comp_pos.as<int32_t>();
     p.rec_dispatch = h->out[GFQ_OUT_REC_DISPATCH].as<double>();
     p.rec_complete = h->out[GFQ_OUT_REC_COMPLETE].as<double>();
     p.rec_pure = h->out[GFQ_OUT_REC_PURE].as<double>();
@@ -891,6 +892,14 @@ int gfq_launch(gfq_handle* h, void* stream) {
     p.hist_lo = h->cfg.hist_lo_s; p.hist_hi = h->cfg.hist_hi_s;
     p.work = h->work.as<int32_t>();
     p.gscratch = h->gscratch.as<unsigned char>();
+    return p;
+}
+
+int gfq_launch(gfq_handle* h, void* stream) {
+    if (!h || !h->prepared) return set_err(GFQ_EINVAL, "gfq_launch: no staged batch");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Params p = make_params(h);
     CK(cudaMemsetAsync(h->work.p, 0, 16, st));
     if (h->cfg.outputs & GFQ_WANT_HIST)
         CK(cudaMemsetAsync(h->out[GFQ_OUT_HIST].p, 0, 8 * h->out_n[GFQ_OUT_HIST], st));
@@ -997,6 +1006,53 @@ int gfq_output_copy(gfq_handle* h, int32_t id, void* host_dst, int64_t bytes) {
 int gfq_output_device_ptr(gfq_handle* h, int32_t id, void** dptr) {
     if (!h || id < 0 || id >= GFQ_OUT_COUNT_ || !dptr) return set_err(GFQ_EINVAL, "gfq_output_device_ptr: bad id");
     *dptr = h->out_n[id] ? h->out[id].p : nullptr;
+    return GFQ_OK;
+}
+
+int gfq_fairness(gfq_handle* h, double window_s, const int32_t* d_max,
+                 const double* report_weight, int64_t n_weights) {
+    if (!h || !h->launched) return set_err(GFQ_EINVAL, "gfq_fairness: no finished batch");
+    if (!(window_s > 0) || (h->n_sims && !d_max))
+        return set_err(GFQ_EINVAL, "gfq_fairness: bad arguments");
+    if ((h->cfg.outputs & (GFQ_WANT_RECORDS | GFQ_WANT_AUDIT)) != (GFQ_WANT_RECORDS | GFQ_WANT_AUDIT))
+        return set_err(GFQ_EINVAL, "gfq_fairness: the batch needs GFQ_WANT_RECORDS | GFQ_WANT_AUDIT");
+    int64_t rows_tab = h->h_tab_off.empty() ? 0 : h->h_tab_off.back();
+    if (n_weights != rows_tab || (rows_tab && !report_weight))
+        return set_err(GFQ_EINVAL, "gfq_fairness: report_weight must cover every flow-table row");
+    for (int i = 0; i < h->n_sims; i++)
+        if (d_max[i] < 1) return set_err(GFQ_EINVAL, "d must be >= 1");
+    for (int64_t i = 0; i < n_weights; i++)
+        if (!(report_weight[i] > 0)) return set_err(GFQ_EINVAL, "weights must be positive");
+    CK(cudaSetDevice(h->device));
+    CK(cudaEventSynchronize(h->ev[2]));
+    const int n = h->n_sims;
+    std::vector<double> ft(std::max(n, 1));
+    if (n) CK(cudaMemcpy(ft.data(), h->out[GFQ_OUT_FINAL_TIME].p, 8 * n, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> woff(n + 1, 0);
+    for (int i = 0; i < n; i++) woff[i + 1] = woff[i] + (int64_t)ceil(ft[i] / window_s) + 2;
+    int rc;
+    if ((rc = alloc_out(h, GFQ_OUT_FAIR_ROWS, 5 * woff[n])) || (rc = alloc_out(h, GFQ_OUT_FAIR_META, 6 * woff[n])) ||
+        (rc = alloc_out(h, GFQ_OUT_FAIR_OFF, n + 1)) || (rc = alloc_out(h, GFQ_OUT_FAIR_COUNT, 3ll * n)))
+        return rc;
+    DBuf dm, rw;
+    if ((rc = dm.ensure(4 * std::max(n, 1))) || (rc = rw.ensure(8 * std::max<int64_t>(n_weights, 1)))) return rc;
+    if (n) CK(cudaMemcpy(dm.p, d_max, 4 * n, cudaMemcpyHostToDevice));
+    if (n_weights) CK(cudaMemcpy(rw.p, report_weight, 8 * n_weights, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->out[GFQ_OUT_FAIR_OFF].p, woff.data(), 8 * (n + 1), cudaMemcpyHostToDevice));
+    const int wpb = 4;
+    int blocks = std::max(1, std::min((n + wpb - 1) / wpb, 4 * h->n_sm));
+    if ((rc = h->fscratch.ensure((size_t)blocks * wpb * 48 * h->L.F))) { dm.release(); rw.release(); return rc; }
+    FairParams fp{};
+    fp.window_s = window_s; fp.d_max = dm.as<int32_t>(); fp.rweight = rw.as<double>();
+    fp.woff = h->out[GFQ_OUT_FAIR_OFF].as<int64_t>();
+    fp.rows = h->out[GFQ_OUT_FAIR_ROWS].as<double>(); fp.meta = h->out[GFQ_OUT_FAIR_META].as<int64_t>();
+    fp.count = h->out[GFQ_OUT_FAIR_COUNT].as<int64_t>(); fp.scratch = h->fscratch.as<unsigned char>();
+    Params p = make_params(h);
+    if (n) k_fairness<<<blocks, wpb * 32>>>(p, fp);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    dm.release(); rw.release();
+    if (e != cudaSuccess) return set_err(GFQ_ECUDA, std::string("k_fairness: ") + cudaGetErrorString(e));
     return GFQ_OK;
 }
 

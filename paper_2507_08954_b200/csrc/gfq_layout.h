@@ -99,6 +99,7 @@ struct Params {
     int64_t* f_count; double* f_mean; double* f_var; double* f_cold;
     // completion-order scratch (always): latency and flow|cold<<31
     double* comp_lat; int32_t* comp_meta;
+    int32_t* comp_pos;             // completion rank -> trace position (GFQ_WANT_RECORDS)
     double* rec_dispatch; double* rec_complete; double* rec_pure;
     int8_t* rec_state; int8_t* rec_device; int32_t* rec_order;
     int32_t* dsp_inv; double* dsp_vt; double* dsp_gvt; int32_t* dsp_qlen; int32_t* dsp_infl;

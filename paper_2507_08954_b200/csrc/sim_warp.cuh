@@ -1036,6 +1036,7 @@ struct WarpSim {
             if (P.outputs & GFQ_WANT_RECORDS) {
                 P.rec_complete[roff + inv] = now;
                 P.rec_order[roff + inv] = k;
+                P.comp_pos[o] = inv;
             }
         }
         if (!SCRIPTED && pt()[fn] - done()[fn] == 0) {     // _backlog_change(-1)

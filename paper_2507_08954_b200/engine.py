@@ -43,6 +43,8 @@ _OUT_DTYPES = {
     _abi.OUT_BACKLOG_TIME: np.float64, _abi.OUT_BACKLOG_META: np.int32,
     _abi.OUT_BACKLOG_COUNT: np.int64, _abi.OUT_EVENT_TIME: np.float64,
     _abi.OUT_EVENT_META: np.int64, _abi.OUT_EVENT_COUNT: np.int64, _abi.OUT_HIST: np.uint64,
+    _abi.OUT_FAIR_ROWS: np.float64, _abi.OUT_FAIR_META: np.int64, _abi.OUT_FAIR_OFF: np.int64,
+    _abi.OUT_FAIR_COUNT: np.int64,
 }
 
 _POLICY = {"mqfq": _abi.POLICY_MQFQ, "fcfs": _abi.POLICY_FCFS, "batch": _abi.POLICY_BATCH,
@@ -184,6 +186,20 @@ class Engine:
         check(self._L.gfq_last_kernel_ms(self._h, C.byref(a), C.byref(b)))
         return float(a.value) + float(b.value)
 
+    def fairness(self, d_max, report_weights, window_s: float = 30.0):
+        """metrics.service_gap_report for every sim of the last batch (which must
+        have been run with WANT_RECORDS | WANT_AUDIT).  d_max: per-sim
+        SchedulerConfig.d_max; report_weights: cfg.weights.get(f, 1.0) for every
+        uploaded flow-table row.  Returns FairnessResult."""
+        dm = np.ascontiguousarray(d_max, dtype=np.int32)
+        rw = np.ascontiguousarray(report_weights, dtype=np.float64)
+        check(self._L.gfq_fairness(self._h, float(window_s), _ptr(dm, C.c_int32),
+                                   _ptr(rw, C.c_double), int(rw.shape[0])))
+        return FairnessResult(self.output(_abi.OUT_FAIR_ROWS).reshape(-1, 5),
+                              self.output(_abi.OUT_FAIR_META).reshape(-1, 6),
+                              self.output(_abi.OUT_FAIR_OFF),
+                              self.output(_abi.OUT_FAIR_COUNT).reshape(-1, 3))
+
     def kernel_times(self, cap: int = 256):
         """(sim_ms, reduce_ms) arrays of the launches since the last call."""
         a = np.zeros(cap, dtype=np.float32)
@@ -223,6 +239,20 @@ class Engine:
     @property
     def rec_off(self):
         return self._rec_off
+
+
+@dataclass
+class FairnessResult:
+    """gfq_fairness outputs; window(i) gives sim i's rows (WindowReport fields)."""
+    rows: np.ndarray        # [windows, 5] w0, service_sum, max_gap, bound, bound_conservative
+    meta: np.ndarray        # [windows, 6] comparable, n_qualified, qual_hash, hi, lo, violated
+    off: np.ndarray         # [sims + 1]
+    count: np.ndarray       # [sims, 3] windows, comparable, violated
+
+    def windows(self, i: int):
+        a = int(self.off[i])
+        k = int(self.count[i, 0])
+        return self.rows[a:a + k], self.meta[a:a + k]
 
 
 class BatchResult:
