@@ -764,7 +764,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     int rc;
     if ((rc = h->sims.ensure(sizeof(gfq_sim) * std::max(n_sims, 1))) || (rc = h->order.ensure(4 * std::max(n_sims, 1))) ||
         (rc = h->sim_foff.ensure(8 * (n_sims + 1))) || (rc = h->sim_roff.ensure(8 * (n_sims + 1))) ||
-        (rc = h->work.ensure(16)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
+        (rc = h->work.ensure(4 * NCLASS)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
         (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))) ||
         (gscr && (rc = h->gscratch.ensure(gscr))) ||
         ((c.outputs & GFQ_WANT_RECORDS) && (rc = h->comp_pos.ensure(4 * std::max<int64_t>(recs, 1)))))
@@ -900,7 +900,7 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)stream;
     Params p = make_params(h);
-    CK(cudaMemsetAsync(h->work.p, 0, 16, st));
+    CK(cudaMemsetAsync(h->work.p, 0, 4 * NCLASS, st));   // one work counter per class
     if (h->cfg.outputs & GFQ_WANT_HIST)
         CK(cudaMemsetAsync(h->out[GFQ_OUT_HIST].p, 0, 8 * h->out_n[GFQ_OUT_HIST], st));
     cudaEvent_t* re = &h->ring[3 * h->ring_next];
