@@ -244,6 +244,7 @@ def run_gfq(args):
               hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S)
     sims = w.sims_array()
     eng.prepare(sims, outputs=outputs, early_exit=True, **kw)
+    info = eng.batch_info()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
     hist_t = None
@@ -346,13 +347,15 @@ def run_gfq(args):
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (gen_zipf Azure-shaped traces, default profiles; per-rank seed blocks)",
-        "config": dict(w.describe, parallelism=f"sims sharded over {world} GPU(s), "
-                       "warp per simulation", l2="flushed (256 MiB write) before every step",
+        "config": dict(w.describe, parallelism=f"sims sharded over {world} GPU(s), " + (
+                           f"CTA ({info['cta_threads']} threads) per simulation"
+                           if info["cta_threads"] else "warp per simulation"),
+                       l2="flushed (256 MiB write) before every step",
                        outputs="per-function stats + latency histograms",
                        dispatch_calls_per_step=calls_per_step, events_per_step=events_per_step,
                        dispatches_per_step_per_gpu=disp_per_step, **scans),
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-        "clocks": clk.summary(), "gpu_launches": args.steps,
+        "clocks": clk.summary(), "gpu_launches": args.steps * info["launches_per_step"],
         "kernel_ms": {"k_sim_mean": kern_ms, "k_reduce_mean": float(statistics.mean(red_ms))
                       if len(red_ms) else None, "step_mean": statistics.mean(step_ms),
                       "step_min": min(step_ms), "step_max": max(step_ms)},

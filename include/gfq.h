@@ -142,6 +142,8 @@ typedef struct gfq_launch_cfg {
 /* gfq_launch_cfg.flags */
 #define GFQ_FLAG_FLOWS_GLOBAL 0x1u /* per-flow state in global scratch (automatic when the
                                       flow count does not fit shared memory)           */
+#define GFQ_FLAG_CTA          0x2u /* one simulation per CTA, every scan split over its
+                                      warps (automatic for large flow counts)          */
 
 #define GFQ_NCOUNTERS 12
 
@@ -258,6 +260,14 @@ int  gfq_last_kernel_ms(gfq_handle* h, float* sim_ms, float* reduce_ms);
  * time the simulation kernel alone over a region of back-to-back launches. */
 #define GFQ_TIMING_RING 256
 int  gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t cap, int32_t* n);
+
+/* How the staged batch will launch: info[0] kernel launches per gfq_launch
+ * (one per active simulation class + the reducer), info[1] simulations per
+ * CTA class mode (0 = warp per simulation, else CTA threads per simulation),
+ * info[2] flows in global scratch (0/1), info[3] simulation warps per CTA in
+ * warp mode, info[4] CTAs of the largest simulation launch.  n = entries
+ * wanted (<= 5). */
+int  gfq_batch_info(gfq_handle* h, int32_t* info, int32_t n);
 
 /* Output access. */
 int  gfq_output_info(gfq_handle* h, int32_t id, int64_t* n_elems, int32_t* elem_bytes);

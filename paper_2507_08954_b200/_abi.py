@@ -17,6 +17,7 @@ DEVMODEL_DEVICESET, DEVMODEL_SCRIPTED = 0, 1
 MAX_DEVICES = 8
 NCOUNTERS = 12
 FLAG_FLOWS_GLOBAL = 0x1
+FLAG_CTA = 0x2
 
 SIM_STATUS = {
     0: "ok",

@@ -166,11 +166,10 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
 }
 
 
-template <int POL, bool ND1>
-__device__ __forceinline__ void run_one(const Params& p, unsigned char* base, unsigned char* fe,
-                                        int lane, int sid) {
+// Per-simulation member setup (every thread that touches the simulation).
+template <int POL, bool ND1, bool CTA>
+__device__ __forceinline__ void sim_setup(WarpSim<POL, ND1, CTA>& w, const Params& p, int sid) {
     constexpr bool G = POL == PB_GENERIC;
-    WarpSim<POL, ND1> w(p, base, fe, lane, sid);
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
     const int t = sim->trace;
@@ -188,18 +187,31 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
     w.ndev = scripted ? 1 : sim->n_devices;
     w.T = sim->t_overrun; w.alpha = sim->alpha; w.dttl = sim->default_ttl_s;
     w.tau_inc = sim->tau_includes_overheads != 0;
+}
 
-    // ---- reset the workspace
+// Zero the per-flow state and container counts (threads t, t+st, ...).
+template <int POL, bool ND1, bool CTA>
+__device__ __forceinline__ void sim_reset_flows(WarpSim<POL, ND1, CTA>& w, const Params& p, int t, int st) {
+    double *vt = w.vt(), *lex = w.lex(), *tau = w.tau(), *iat = w.iat(), *larr = w.larr();
+    int *pt = w.pt(), *ph = w.ph(), *infl = w.infl(), *head = w.head(), *done = w.done(), *pend = w.pend();
+    uint8_t* fst = w.fst();
+    for (int f = t; f < w.nf; f += st) {
+        vt[f] = 0.0; lex[f] = 0.0; tau[f] = 0.0; iat[f] = 0.0; larr[f] = 0.0;
+        pt[f] = 0; ph[f] = 0; infl[f] = 0; head[f] = -1; done[f] = 0; pend[f] = 0; fst[f] = 0;
+    }
+    uint16_t* cnt = (uint16_t*)(w.fe + p.L.o_cnt);
+    for (int i = t; i < 3 * w.ndev * p.L.F; i += st) cnt[i] = 0;
+}
+
+// Device state reset, the event loop and the per-simulation outputs (one warp).
+template <int POL, bool ND1, bool CTA>
+__device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params& p, int sid) {
+    constexpr bool G = POL == PB_GENERIC;
+    const gfq_sim* sim = w.sim;
+    const int lane = w.lane;
+    unsigned char* base = w.sm;
+    const bool scripted = G && w.scripted_;
     {
-        double *vt = w.vt(), *lex = w.lex(), *tau = w.tau(), *iat = w.iat(), *larr = w.larr();
-        int *pt = w.pt(), *ph = w.ph(), *infl = w.infl(), *head = w.head(), *done = w.done(), *pend = w.pend();
-        uint8_t* fst = w.fst();
-        for (int f = lane; f < w.nf; f += 32) {
-            vt[f] = 0.0; lex[f] = 0.0; tau[f] = 0.0; iat[f] = 0.0; larr[f] = 0.0;
-            pt[f] = 0; ph[f] = 0; infl[f] = 0; head[f] = -1; done[f] = 0; pend[f] = 0; fst[f] = 0;
-        }
-        uint16_t* cnt = (uint16_t*)(fe + p.L.o_cnt);
-        for (int i = lane; i < 3 * w.ndev * p.L.F; i += 32) cnt[i] = 0;
         if (lane < w.ndev) {
             int d = lane;
             int* dvi = (int*)(base + p.L.o_dvi) + d * DV_NI;
@@ -261,6 +273,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
     if (w.n > 0 && !scripted) w.push(w.period, EV_TICK, 0);
 
     w.run();
+    if (CTA) w.cta_release();
 
     if (lane == 0) {
         p.status[sid] = w.status;
@@ -283,6 +296,16 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
     __syncwarp();
 }
 
+template <int POL, bool ND1>
+__device__ __forceinline__ void run_one(const Params& p, unsigned char* base, unsigned char* fe,
+                                        int lane, int sid) {
+    WarpSim<POL, ND1> w(p, base, fe, lane, sid);
+    sim_setup(w, p, sid);
+    sim_reset_flows(w, p, lane, 32);
+    __syncwarp();
+    sim_run(w, p, sid);
+}
+
 #ifndef GFQ_MINB
 #define GFQ_MINB 4
 #endif
@@ -301,6 +324,36 @@ __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ P
         idx = __shfl_sync(FULLMASK, idx, 0);
         if (idx >= p.n_sims) break;
         run_one<POL, ND1>(p, base, fe, lane, p.order[idx]);
+    }
+}
+
+// CTA-per-simulation engine for large flow counts (BASELINE C4: 4096
+// functions): one simulation per CTA, its whole workspace in the CTA's shared
+// memory (or the flow/event part in a per-CTA global slice, FG).  Warp 0 runs
+// the event loop; warps 1.. serve its flow scans and event-pool argmins
+// (WarpSim::cta_scan / helper_loop, named barriers 1 and 2).
+template <bool FG>
+__global__ void __launch_bounds__(GFQ_CTA_THREADS, 1) k_sim_cta(const __grid_constant__ Params p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_idx;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* fe = FG ? p.gscratch + (size_t)blockIdx.x * p.L.fe_bytes : smem;
+    unsigned char* base = FG ? smem : smem + p.L.fe_bytes;
+    for (;;) {
+        if (threadIdx.x == 0) s_idx = atomicAdd(p.work, 1);
+        __syncthreads();
+        const int idx = s_idx;
+        __syncthreads();
+        if (idx >= p.n_sims) break;
+        const int sid = p.order[idx];
+        WarpSim<PB_GENERIC, false, true> w(p, base, fe, lane, sid);
+        w.wid = warp; w.nthr = blockDim.x; w.use_inf_ = 0;
+        sim_setup(w, p, sid);
+        sim_reset_flows(w, p, threadIdx.x, blockDim.x);
+        __syncthreads();
+        if (warp == 0) sim_run(w, p, sid);
+        else w.helper_loop();
+        __syncthreads();
     }
 }
 
@@ -367,9 +420,10 @@ __global__ void k_trace_index(const int32_t* flow, const int64_t* trace_off, con
 using namespace gfq;
 
 // the k_sim instantiation of each kernel class (see gfq_prepare)
-enum { NCLASS = 6 };
+enum { NCLASS = 7, CLASS_CTA = 6 };
 static const void* class_kernel(int k, bool flows_global) {
     switch (k) {
+        case CLASS_CTA: return flows_global ? (const void*)k_sim_cta<true> : (const void*)k_sim_cta<false>;
         case 1: return (const void*)k_sim<PB_MQFQ, false, false>;
         case 2: return (const void*)k_sim<PB_MQFQ, true, false>;
         case 3: return (const void*)k_sim<PB_FCFS, true, false>;
@@ -439,6 +493,7 @@ struct gfq_handle {
     gfq_launch_cfg cfg{};
     Layout L{};
     int wpb = 0, rwpb = 4, rblocks = 1;
+    int cta_threads = 0, cta_min = 64;
     bool rglobal = false;
     int ccount[NCLASS] = {0}, cblocks[NCLASS] = {0};   // per kernel class
     bool prepared = false;
@@ -698,10 +753,34 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     L.ND = nd; L.P = P; L.R = R; L.S = S;
     L.E = c.event_capacity > 0 ? c.event_capacity : std::max(64, ((2 * max_nf + 2 * R * nd + 32) + 31) & ~31);
     L.flows_global = 0;
+    L.cta = 0;
     layout_finish(L);
+    // Large flow counts (fewer than 4 warp-simulations' workspaces fit an SM's
+    // shared memory, or GFQ_FLAG_CTA): one simulation per CTA, its scans split
+    // over the CTA's warps.  The CTA gets 512 threads (256 when two such
+    // simulations fit an SM).
+    int cta_threads = 0;
+    if ((c.flags & GFQ_FLAG_CTA) || (size_t)4 * L.bytes > h->smem_optin) {
+        L.cta = 1;
+        layout_finish(L);
+        cta_threads = (size_t)2 * L.bytes <= h->smem_optin ? 256 : GFQ_CTA_THREADS;
+    }
     // flow counts whose per-simulation state does not fit in shared memory
     // (or GFQ_FLAG_FLOWS_GLOBAL) put the flow/event part in global scratch
-    if ((c.flags & GFQ_FLAG_FLOWS_GLOBAL) || (size_t)L.bytes > h->smem_optin) {
+    const size_t smem_avail = h->smem_optin - (L.cta ? 64 : 0);     // CTA mode: + static s_idx
+    // CTA mode: rather than spill the flow state to global memory, trim the
+    // default event capacity (2 slots per flow) to what fits, down to 1 slot
+    // per flow + 2 per token + 64; a simulation that still overflows reports
+    // GFQ_SIM_EVENT_OVERFLOW (callers re-run it with a larger event_capacity)
+    if (L.cta && c.event_capacity <= 0 && (size_t)L.bytes > smem_avail) {
+        const int32_t over = (int32_t)(((size_t)L.bytes - smem_avail + 15) / 16);
+        const int32_t e_fit = (L.E - over) & ~31;
+        if (e_fit >= max_nf + 2 * R * nd + 64) {
+            L.E = e_fit;
+            layout_finish(L);
+        }
+    }
+    if ((c.flags & GFQ_FLAG_FLOWS_GLOBAL) || (size_t)L.bytes > smem_avail) {
         L.flows_global = 1;
         layout_finish(L);
     }
@@ -718,7 +797,9 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     for (int i = 0; i < n_sims; i++) {
         const gfq_sim& s = sims[i];
         int k = 0;
-        if (!logs && !L.flows_global && s.device_model == GFQ_DEVMODEL_DEVICESET) {
+        if (L.cta) {
+            k = CLASS_CTA;
+        } else if (!logs && !L.flows_global && s.device_model == GFQ_DEVMODEL_DEVICESET) {
             if (s.n_devices == 1) {
                 k = s.policy == GFQ_POLICY_MQFQ ? 2
                   : (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) ? 3
@@ -732,21 +813,24 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     }
     int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, 4) : 4;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
+    if (L.cta) wpb = 1;                       // one simulation (workspace) per CTA
     size_t smem = (size_t)wpb * L.bytes;
     int cblocks[NCLASS] = {0};
     for (int k = 0; k < NCLASS; k++) {
         if (!ccount[k]) continue;
         const void* kfn = class_kernel(k, L.flows_global);
+        const int threads = k == CLASS_CTA ? cta_threads : wpb * 32;
+        const int per_cta = k == CLASS_CTA ? 1 : wpb;   // simulations in flight per CTA
         CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // all of the unified L1/shared array to shared memory: occupancy is bounded
         // by per-warp simulation state; the kernel's global traffic is tiny
         CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 (int)cudaSharedmemCarveoutMaxShared));
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, wpb * 32, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, smem));
         if (per_sm < 1) return set_err(GFQ_EINVAL, "gfq_prepare: kernel does not fit on an SM");
         int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
-        cblocks[k] = std::max(1, std::min(blocks, (ccount[k] + wpb - 1) / wpb));
+        cblocks[k] = std::max(1, std::min(blocks, (ccount[k] + per_cta - 1) / per_cta));
     }
     // reducer: 60 B of scratch per flow per warp, shared memory or global
     int rwpb = 4;
@@ -758,7 +842,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
                                 (int)(rwpb * 60 * L.F)));
     size_t gscr = 0;
     if (L.flows_global)
-        for (int k = 0; k < NCLASS; k++) gscr = std::max(gscr, (size_t)cblocks[k] * wpb * L.fe_bytes);
+        for (int k = 0; k < NCLASS; k++) gscr = std::max(gscr, (size_t)cblocks[k] * (k == CLASS_CTA ? 1 : wpb) * L.fe_bytes);
     if (rglobal) gscr = std::max(gscr, (size_t)rblocks * rwpb * 60 * L.F);
 
     int rc;
@@ -825,6 +909,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->cfg = c;
     h->L = L;
     h->wpb = wpb;
+    h->cta_threads = cta_threads;
+    h->cta_min = (c.flags & GFQ_FLAG_CTA) ? 0 : 64;
     h->rwpb = rwpb;
     h->rblocks = rblocks;
     h->rglobal = rglobal;
@@ -853,6 +939,7 @@ static Params make_params(gfq_handle* h) {
     p.dcfg = h->dcfg.as<gfq_device_cfg>(); p.execs = h->execs.as<double>();
     p.sim_foff = h->sim_foff.as<int64_t>(); p.sim_roff = h->sim_roff.as<int64_t>();
     p.L = h->L;
+    p.cta_min = h->cta_min;
     p.outputs = h->cfg.outputs;
     p.early_exit = h->cfg.early_exit;
     p.status = h->out[GFQ_OUT_STATUS].as<int32_t>();
@@ -915,7 +1002,7 @@ int gfq_launch(gfq_handle* h, void* stream) {
             pk.order = p.order + off;
             pk.n_sims = h->ccount[k];
             pk.work = p.work + k;
-            dim3 g(h->cblocks[k]), b(h->wpb * 32);
+            dim3 g(h->cblocks[k]), b(k == CLASS_CTA ? h->cta_threads : h->wpb * 32);
             void* args[] = {&pk};
             CK(cudaLaunchKernel(class_kernel(k, h->L.flows_global), g, b, args, smem, st));
             off += h->ccount[k];
@@ -984,6 +1071,16 @@ int gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t cap
     }
     *n = cnt;
     h->ring_count = 0;
+    return GFQ_OK;
+}
+
+int gfq_batch_info(gfq_handle* h, int32_t* info, int32_t n) {
+    if (!h || !h->prepared || !info || n < 0 || n > 5) return set_err(GFQ_EINVAL, "gfq_batch_info: bad arguments");
+    int32_t v[5] = {0, h->L.cta ? h->cta_threads : 0, h->L.flows_global, h->wpb, 0};
+    for (int k = 0; k < NCLASS; k++)
+        if (h->ccount[k]) { v[0]++; v[4] = std::max(v[4], h->cblocks[k]); }
+    if (h->n_sims > 0) v[0]++;                             // k_reduce
+    for (int i = 0; i < n; i++) info[i] = v[i];
     return GFQ_OK;
 }
 

@@ -37,6 +37,19 @@ enum { DG_MAXEV = 0, DG_GSCAN, DG_RSCAN, DG_CSCAN, DG_TICKS, DG_WHIT, DG_WMISS, 
 // event kinds (engine.py:20-23)
 enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };
 
+// CTA mode: the leader warp's scan command and the per-warp partial argmins
+// (lexicographic (k, s, i)) the helper warps return.
+enum { CTA_MAXW = 32 };
+#define GFQ_CTA_THREADS 512        // threads of a CTA-mode simulation (max)
+struct CtaCmd {
+    int32_t op, nf, nev, iarg;     // scan kind, flow count, event slots, use_inf
+    int32_t newly_n, flag, pad0, pad1;
+    double gvt, now;
+    unsigned long long pk[CTA_MAXW];
+    uint32_t ps[CTA_MAXW];
+    int32_t pi[CTA_MAXW];
+};
+
 struct Layout {
     int32_t F;      // flow slots (multiple of 32)
     int32_t E;      // dynamic event slots (completions + keep-alive expiries)
@@ -60,11 +73,15 @@ struct Layout {
     int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u64[ND][WMEMO], f64[ND][WMEMO]
     int32_t o_diag;                                      // u32[DG_N]
     int32_t o_newly;                                     // i32[NEWLY_CAP]
+    int32_t o_cta;                                       // CtaCmd (CTA-per-simulation mode only)
     int32_t dev_bytes;
     // the fe part lives in shared memory in front of the device part, or (for
     // flow counts whose state does not fit) in a per-warp global scratch slice
     int32_t flows_global;
-    int32_t bytes;                                       // shared bytes per warp
+    // CTA-per-simulation mode (large flow counts): one simulation per CTA,
+    // warp 0 runs the event loop, the other warps join its O(F) scans
+    int32_t cta;
+    int32_t bytes;                                       // shared bytes per warp (per CTA in CTA mode)
 };
 
 struct Params {
@@ -108,6 +125,7 @@ struct Params {
     double* event_time; int64_t* event_meta; int64_t* event_count; int64_t event_log_cap;
     unsigned long long* hist; int32_t hist_rows, hist_bins; double hist_lo, hist_hi;
     int32_t* work;                 // work-queue counter
+    int32_t cta_min;               // CTA mode: scans shorter than this stay on the leader warp
     unsigned char* gscratch;       // per-warp fe slices when L.flows_global
 };
 
@@ -133,6 +151,7 @@ inline void layout_finish(Layout& L) {
     L.o_wdict = take(8 * WDICT * ND); L.o_wkey = take(8 * WMEMO * ND); L.o_wval = take(8 * WMEMO * ND);
     L.o_diag = take(4 * DG_N);
     L.o_newly = take(4 * NEWLY_CAP);
+    L.o_cta = L.cta ? take((int32_t)sizeof(CtaCmd)) : 0;
     L.dev_bytes = o;
     L.bytes = L.flows_global ? L.dev_bytes : L.fe_bytes + L.dev_bytes;
 }

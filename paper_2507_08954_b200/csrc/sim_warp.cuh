@@ -132,7 +132,26 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 // and the audit / event logs; the others are one policy on a DeviceSet.
 enum { PB_GENERIC = 0, PB_MQFQ = 1, PB_FCFS = 2, PB_BATCH = 3, PB_SJF = 4 };
 
-template <int POL, bool ND1>
+// CTA-mode scan kinds (the leader warp's command to the helper warps)
+enum { OP_EXIT = 0, OP_GVT, OP_REFRESH, OP_CAND, OP_BATCH, OP_SJF, OP_EVMIN };
+
+// lexicographic (k, s, i) argmin candidate
+struct Arg { u64 k; uint32_t s; int i; };
+FI Arg arg_none() { Arg a; a.k = ~0ull; a.s = 0xffffffffu; a.i = 0x7fffffff; return a; }
+FI Arg warp_argmin(Arg a) {
+    Arg r;
+    r.k = wmin64(a.k);
+    r.s = wmin32(a.k == r.k ? a.s : 0xffffffffu);
+    r.i = (int)wmin32(a.k == r.k && a.s == r.s ? (unsigned)a.i : 0x7fffffffu);
+    return r;
+}
+// named barrier over the n threads of the simulation's CTA
+FI void cta_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// CTA = one simulation per CTA (large flow counts): warp 0
+// (the leader) runs everything below; the O(F) flow scans and the event-pool
+// argmin are split over all the CTA's warps (cta_scan / helper_loop).
+template <int POL, bool ND1, bool CTA = false>
 struct WarpSim {
     static constexpr bool G = POL == PB_GENERIC;
     const Params& P;
@@ -232,6 +251,112 @@ struct WarpSim {
     FI WarpSim(const Params& p, unsigned char* s, unsigned char* f, int l, int id)
         : P(p), sm(s), fe(f), lane(l), sid(id) {}
 
+    // ---- CTA mode
+    int wid, nthr;                     // warp index in the CTA, CTA threads
+    int use_inf_;                      // candidate order uses in_flight (helpers' copy)
+    FI CtaCmd* cmd() const { return (CtaCmd*)(sm + P.L.o_cta); }
+    FI bool cta_on(int n) const { return CTA && n >= P.cta_min; }
+
+    // This warp's share of a scan (every warp of the CTA runs it; flows
+    // f = wid*32 + lane + k*nthr), reduced over the warp.
+    FI Arg cta_part(int op) {
+        Arg a = arg_none();
+        const int lim = op == OP_EVMIN ? nev : nf;
+        #pragma unroll 1
+        for (int b = wid * 32; b < lim; b += nthr) {
+            const int f = b + lane;
+            const bool in = f < lim;
+            if (op == OP_GVT) {
+                if (in && pt()[f] - done()[f] > 0) { u64 k = okey(vt()[f]); if (k < a.k) a.k = k; }
+            } else if (op == OP_CAND) {
+                if (in) {
+                    int pe = pend()[f];
+                    if (pe > 0 && vt()[f] - gvt <= T) {
+                        unsigned inf = use_inf_ ? (unsigned)infl()[f] : 0u;
+                        u64 k = ((u64)inf << 48) | ((u64)(0xffffffffu - (unsigned)pe) << 16) | (u64)f;
+                        if (k < a.k) a.k = k;
+                    }
+                }
+            } else if (op == OP_BATCH) {
+                if (in && pend()[f] > 0) a.k = min(a.k, (u64)(unsigned)head()[f]);
+            } else if (op == OP_SJF) {
+                if (in && pend()[f] > 0) {
+                    u64 k = okey(tau()[f]);
+                    if (k < a.k) { a.k = k; a.i = f; }
+                }
+            } else if (op == OP_EVMIN) {
+                if (in) {
+                    u64 k = okey(ev_t()[f]); uint32_t q = ev_seq()[f];
+                    if (k < a.k || (k == a.k && q < a.s)) { a.k = k; a.s = q; a.i = f; }
+                }
+            } else {                                        // OP_REFRESH
+                bool idle = false, mk = false;
+                uint8_t st = 0;
+                double le = 0.0, tt = 0.0;
+                if (in) {
+                    st = fst()[f];
+                    idle = (st & (FL_CREATED | FL_INACTIVE)) == FL_CREATED && pt()[f] - done()[f] == 0;
+                    if (idle) { le = lex()[f]; tt = ttl(f); mk = now - le >= tt; }
+                }
+                if (!SCRIPTED) {         // append to the newly-inactive list (order is immaterial)
+                    unsigned bm = __ballot_sync(FULLMASK, mk);
+                    if (bm) {
+                        int pos0 = 0;
+                        if (lane == 0) pos0 = atomicAdd(&cmd()->newly_n, __popc(bm));
+                        pos0 = __shfl_sync(FULLMASK, pos0, 0);
+                        int pos = pos0 + __popc(bm & ((1u << lane) - 1));
+                        if (mk && pos < NEWLY_CAP) NEWLY()[pos] = f;
+                    }
+                }
+                if (mk) {
+                    fst()[f] = (uint8_t)(st | FL_INACTIVE | (SCRIPTED ? 0 : FL_NEWLY));
+                    cmd()->flag = 1;
+                } else if (idle) {
+                    u64 k = okey(expiry_lb(le, tt));
+                    if (k < a.k) a.k = k;
+                }
+            }
+        }
+        return warp_argmin(a);
+    }
+
+    // Leader: publish the command, do warp 0's share, combine every warp's.
+    FI Arg cta_scan(int op) {
+        CtaCmd* c = cmd();
+        __syncwarp();
+        if (lane == 0) {
+            c->op = op; c->nf = nf; c->nev = nev; c->iarg = use_inf_;
+            c->gvt = gvt; c->now = now;
+        }
+        cta_bar(1, nthr);
+        Arg a = cta_part(op);
+        if (lane == 0) { c->pk[0] = a.k; c->ps[0] = a.s; c->pi[0] = a.i; }
+        cta_bar(2, nthr);
+        Arg b = arg_none();
+        if (lane < (nthr >> 5)) { b.k = c->pk[lane]; b.s = c->ps[lane]; b.i = c->pi[lane]; }
+        return warp_argmin(b);
+    }
+
+    // Helper warps: serve the leader's scans until it sends OP_EXIT.
+    FI void helper_loop() {
+        CtaCmd* c = cmd();
+        #pragma unroll 1
+        for (;;) {
+            cta_bar(1, nthr);
+            const int op = c->op;
+            if (op == OP_EXIT) break;
+            nf = c->nf; nev = c->nev; use_inf_ = c->iarg; gvt = c->gvt; now = c->now;
+            Arg a = cta_part(op);
+            if (lane == 0) { c->pk[wid] = a.k; c->ps[wid] = a.s; c->pi[wid] = a.i; }
+            cta_bar(2, nthr);
+        }
+    }
+    FI void cta_release() {            // leader, end of the simulation
+        __syncwarp();
+        if (lane == 0) cmd()->op = OP_EXIT;
+        cta_bar(1, nthr);
+    }
+
     FI void fail(int st) { if (!status) status = st; }
 #define UNLIKELY(x) __builtin_expect(!!(x), 0)
     FI double ttl(int f) const {                          // FlowQueue.ttl, core.py:140-152
@@ -259,6 +384,13 @@ struct WarpSim {
     }
 
     FI void pool_min() {                                  // lane-parallel argmin
+        if (cta_on(nev)) {
+            Arg a = cta_scan(OP_EVMIN);
+            pmin_ok = true;
+            if (a.i == 0x7fffffff) { pmin_slot = -1; return; }
+            pmin_slot = a.i; pmin_t = from_key(a.k); pmin_seq = a.s;
+            return;
+        }
         u64 bt = ~0ull; uint32_t bs = 0xffffffffu; int bslot = -1;
         #pragma unroll 1
         for (int i = lane; i < nev; i += 32) {
@@ -661,6 +793,11 @@ struct WarpSim {
     // (A) recompute_global_vt, mqfq.py:114-127.  INACTIVE => not backlogged,
     // so the filter is "backlogged"; the minimum is cached (gmin).
     FI void recompute_gvt() {
+        if (!gmin_ok && cta_on(nf)) {
+            diag(DG_GSCAN);
+            gmin = cta_scan(OP_GVT).k;
+            gmin_ok = true;
+        }
         if (!gmin_ok) {
             diag(DG_GSCAN);
             u64 bk = ~0ull;
@@ -690,6 +827,16 @@ struct WarpSim {
     FI void refresh_states() {
         if (now < idle_lb) return;
         diag(DG_RSCAN);
+        if (cta_on(nf)) {
+            CtaCmd* c = cmd();
+            __syncwarp();
+            if (lane == 0) { c->newly_n = newly_n; c->flag = 0; }
+            Arg a = cta_scan(OP_REFRESH);
+            newly_n = c->newly_n;
+            if (c->flag && !SCRIPTED) any_newly = true;
+            idle_lb = a.k == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_key(a.k);
+            return;
+        }
         u64 lbk = ~0ull;
         bool newly = false;
         #pragma unroll 1
@@ -728,6 +875,11 @@ struct WarpSim {
     FI int mqfq_candidate() {
         diag(DG_CSCAN);
         bool use_inf = max_effective_d() != 1;
+        if (cta_on(nf)) {
+            use_inf_ = use_inf;
+            u64 m = cta_scan(OP_CAND).k;
+            return m == ~0ull ? -1 : (int)(m & 0xffffu);
+        }
         u64 bk = ~0ull;
         #pragma unroll 1
         for (int f = lane; f < nf; f += 32) {
@@ -749,6 +901,10 @@ struct WarpSim {
         if (dr >= 0 && (pend()[dr] > 0 || infl()[dr] > 0))
             return pend()[dr] == 0 ? -1 : dr;                // hold for late arrivals
         diag(DG_CSCAN);
+        if (cta_on(nf)) {
+            u64 m = cta_scan(OP_BATCH).k;
+            return m == ~0ull ? -1 : flw((int)m);
+        }
         unsigned bk = 0xffffffffu;
         #pragma unroll 1
         for (int f = lane; f < nf; f += 32)
@@ -760,6 +916,10 @@ struct WarpSim {
     // SjfPolicy.dispatch, policies.py:245-262: min tau.mean, name order on ties
     FI int sjf_candidate() {
         diag(DG_CSCAN);
+        if (cta_on(nf)) {
+            Arg a = cta_scan(OP_SJF);
+            return a.k == ~0ull ? -1 : a.i;
+        }
         u64 bk = ~0ull; int bf = 0x7fffffff;
         #pragma unroll 1
         for (int f = lane; f < nf; f += 32)

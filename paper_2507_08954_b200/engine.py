@@ -200,6 +200,13 @@ class Engine:
                               self.output(_abi.OUT_FAIR_OFF),
                               self.output(_abi.OUT_FAIR_COUNT).reshape(-1, 3))
 
+    def batch_info(self) -> dict:
+        """gfq_batch_info of the staged batch."""
+        v = np.zeros(5, dtype=np.int32)
+        check(self._L.gfq_batch_info(self._h, _ptr(v, C.c_int32), 5))
+        return {"launches_per_step": int(v[0]), "cta_threads": int(v[1]),
+                "flows_global": bool(v[2]), "warps_per_block": int(v[3]), "ctas": int(v[4])}
+
     def kernel_times(self, cap: int = 256):
         """(sim_ms, reduce_ms) arrays of the launches since the last call."""
         a = np.zeros(cap, dtype=np.float32)

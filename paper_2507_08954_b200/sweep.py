@@ -116,8 +116,9 @@ def c4(seed_base: int = 1, n_seeds: int = 4, duration: float = 1800.0, rate: flo
     """BASELINE C4 (configs[3]): 4096 functions per simulation (Zipf 0.5, ~2.1k
     touched in 1800 s at 2 rps), heterogeneous memory (mem_mb by rank mod 5),
     16 GB device, D=4, container pool 32 or 256 -> cold starts, host-warm
-    prefetch and LRU swap all exercised.  Per-flow state exceeds shared
-    memory, so these run the flows-in-global build."""
+    prefetch and LRU swap all exercised.  A simulation's workspace (~220 KB)
+    takes a whole SM's shared memory, so these run the CTA-per-simulation
+    build (k_sim_cta, 512 threads, scans split over 16 warps)."""
     from .core import FunctionProfile
     n_fn = 4096
     base = default_profiles(n_fn)
@@ -206,7 +207,7 @@ def build(name: str, rank: int = 0, **kw) -> Workload:
         n = kw.get("n_seeds", 456)
         return c2(seed_base=1 + rank * n, n_seeds=n)
     if name == "c4":
-        n = kw.get("n_seeds", 4)
+        n = kw.get("n_seeds", 37)          # 37 seeds x 2 pools x 2 policies = 148 sims, 1 per SM
         return c4(seed_base=1 + rank * n, n_seeds=n)
     if name == "c5":
         n = kw.get("n_seeds", 1563)

@@ -121,6 +121,24 @@ def test_flows_global_build(engine):
     assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
 
 
+@pytest.mark.parametrize("flags", ["cta", "cta+global"])
+def test_cta_build(engine, flags):
+    """The CTA-per-simulation build (one simulation per CTA, scans split over
+    its warps; automatic for large flow counts), forced on every golden case
+    with every scan on the CTA path (cta_min = 0), with the workspace in
+    shared memory and with the flow/event part in global scratch."""
+    from gpu_harness import compare_to_golden, run_cases
+    from paper_2507_08954_b200 import _abi
+    cases = all_cases()
+    f = _abi.FLAG_CTA | (_abi.FLAG_FLOWS_GLOBAL if "global" in flags else 0)
+    outs, _ = run_cases(cases, engine, early_exit=False, event_log_cap=65536,
+                        audit_util_cap=16384, flags=f)
+    gold = golden()
+    bad = {c["name"]: m for c, o in zip(cases, outs)
+           if (m := compare_to_golden(o, gold[c["name"]]))}
+    assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
+
+
 def test_c4_large_flow_sims_match_oracle(engine):
     """BASELINE C4: 4096 functions per simulation (2.1k touched), pool 32/256,
     heterogeneous memory, MQFQ + FCFS: flows-in-global build vs the oracle."""
