@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--seeds", type=int, default=0, help="seeds per GPU (default: the config's)")
+    ap.add_argument("--event-capacity", type=int, default=0,
+                    help="dynamic event slots per simulation (0 = the engine's default)")
     return ap.parse_args()
 
 
@@ -241,7 +243,8 @@ def run_gfq(args):
     w.upload(eng)
     outputs = _abi.WANT_STATS | _abi.WANT_HIST
     kw = dict(hist_groups=w.groups, hist_rows=w.hist_rows, hist_bins=sweep.HIST_BINS,
-              hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S)
+              hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S,
+              event_capacity=args.event_capacity)
     sims = w.sims_array()
     eng.prepare(sims, outputs=outputs, early_exit=True, **kw)
     info = eng.batch_info()

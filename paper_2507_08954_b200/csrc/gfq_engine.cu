@@ -30,6 +30,10 @@
 #include "sim_warp.cuh"
 #include "fairness.cuh"
 
+#ifndef GFQ_TIMELINE
+#define GFQ_TIMELINE 0      // diagnostic build: per-simulation start/end time and SM in the counters
+#endif
+
 namespace gfq {
 
 // ----------------------------------------------------------------------------
@@ -60,7 +64,11 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
         cnt[f] = 0; coldc[f] = 0; first[f] = -1; vcnt[f] = 0;
     }
     __syncwarp();
-    const double* lat = p.comp_lat + roff;
+    // completion stream: completion time, trace position, flow | cold << 31;
+    // latency = complete - arrival (InvocationRecord.latency_s)
+    const double* ctime = p.comp_lat + roff;
+    const int32_t* cpos = p.comp_pos + roff;
+    const double* arrival = p.arrival + p.trace_off[sim->trace];
     const int32_t* meta = p.comp_meta + roff;
     int nfirst = 0;
     int colds = 0;
@@ -71,7 +79,7 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
     for (int base = 0; base < nrec; base += 32) {
         int k = base + lane;
         double x = 0.0; int32_t m = 0;
-        if (k < nrec) { x = lat[k]; m = meta[k]; }
+        if (k < nrec) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
         if (want_hist && k < nrec) {
             int fn = m & 0x7fffffff;
             int b = x > 0.0 ? (int)floor((log(x) - hl0) * hscale) : 0;
@@ -117,7 +125,7 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
     for (int base = 0; base < nrec; base += 32) {
         int k = base + lane;
         double x = 0.0; int32_t m = 0;
-        if (k < nrec) { x = lat[k]; m = meta[k]; }
+        if (k < nrec) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
         int nb = min(32, nrec - base);
         for (int j = 0; j < nb; j++) {
             double xj = __shfl_sync(FULLMASK, x, j);
@@ -211,6 +219,10 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
     const int lane = w.lane;
     unsigned char* base = w.sm;
     const bool scripted = G && w.scripted_;
+#if GFQ_TIMELINE
+    unsigned long long tl0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
+#endif
     {
         if (lane < w.ndev) {
             int d = lane;
@@ -234,6 +246,8 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
                 dvd[DD_LKEY] = __longlong_as_double(-1ll);      // ~0: no previous window
                 u64* wk = (u64*)(base + p.L.o_wkey) + d * WMEMO;
                 for (int k = 0; k < WMEMO; k++) wk[k] = ~0ull;   // no valid key has all bits set
+                u64* wd = (u64*)(base + p.L.o_wdict) + d * WDICT;
+                for (int k = 0; k < WDICT; k++) wd[k] = ~0ull;   // empty intern slots
             }
         }
         uint32_t* dg = (uint32_t*)(base + p.L.o_diag);
@@ -284,6 +298,13 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
         c[C_MAXEV] = dg[DG_MAXEV]; c[C_GSCAN] = dg[DG_GSCAN]; c[C_RSCAN] = dg[DG_RSCAN];
         c[C_CSCAN] = dg[DG_CSCAN]; c[C_TICKS] = dg[DG_TICKS]; c[C_WHIT] = dg[DG_WHIT];
         c[C_WMISS] = dg[DG_WMISS]; c[C_QUIET] = dg[DG_QUIET];
+#if GFQ_TIMELINE
+        // -DGFQ_TIMELINE=1 diagnostic build: start / end (ns) and SM of each simulation
+        unsigned long long tl1; unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        c[C_GSCAN] = (int64_t)tl0; c[C_RSCAN] = (int64_t)tl1; c[C_CSCAN] = smid;
+#endif
         p.final_time[sid] = w.now;
         if (p.outputs & GFQ_WANT_AUDIT) p.backlog_count[sid] = w.n_backlog;
         if (p.outputs & GFQ_WANT_EVENTS) p.event_count[sid] = w.n_evlog;
@@ -309,6 +330,7 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
 #ifndef GFQ_MINB
 #define GFQ_MINB 4
 #endif
+
 template <int POL, bool ND1, bool FG>
 __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -339,6 +361,7 @@ __global__ void __launch_bounds__(GFQ_CTA_THREADS, 1) k_sim_cta(const __grid_con
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* fe = FG ? p.gscratch + (size_t)blockIdx.x * p.L.fe_bytes : smem;
     unsigned char* base = FG ? smem : smem + p.L.fe_bytes;
+    if (warp == 0) ring_init(base, p.L, lane);
     for (;;) {
         if (threadIdx.x == 0) s_idx = atomicAdd(p.work, 1);
         __syncthreads();
@@ -471,6 +494,7 @@ struct gfq_handle {
     int device = 0;
     int n_sm = 0;
     size_t smem_optin = 0;
+    size_t smem_per_sm = 0;
     // traces
     DBuf arrival, flow, trace_off, trace_nf, foff_off, foff, fpos;
     std::vector<int64_t> h_trace_off;
@@ -539,6 +563,9 @@ int gfq_create(int device, gfq_handle** out) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     h->smem_optin = (size_t)optin;
+    int per_sm_smem = 0;
+    CK(cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+    h->smem_per_sm = (size_t)per_sm_smem;
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     h->ring.resize(3 * GFQ_TIMING_RING);
     for (auto& e : h->ring) CK(cudaEventCreate(&e));
@@ -589,7 +616,10 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
         max_nf = std::max(max_nf, n_flows[t]);
     }
     int rc;
-    if ((rc = h->arrival.ensure(8 * total)) || (rc = h->flow.ensure(4 * total)) ||
+    // padded to whole 32-entry chunks: k_sim streams the traces in by TMA
+    // bulk copies of aligned 32-entry chunks (WarpSim::ring_issue)
+    const int64_t padded = ((total + 31) & ~(int64_t)31) + 32;
+    if ((rc = h->arrival.ensure(8 * padded)) || (rc = h->flow.ensure(4 * padded)) ||
         (rc = h->fpos.ensure(4 * total)) || (rc = h->trace_off.ensure(8 * (n_traces + 1))) ||
         (rc = h->trace_nf.ensure(4 * std::max(n_traces, 1))) ||
         (rc = h->foff_off.ensure(8 * (n_traces + 1))) || (rc = h->foff.ensure(4 * foff_off[n_traces])))
@@ -745,7 +775,14 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         max_n = std::max<int>(max_n, (int)n);
         foffs[i + 1] = foffs[i] + nf;
         roffs[i + 1] = roffs[i] + n;
-        cost[i] = (double)n * (1.0 + nf / 32.0) * (s.policy == GFQ_POLICY_MQFQ ? 2.0 : 1.0);
+        // LPT cost estimate: events grow with the trace, the flow scans with
+        // nf, and the backlog (hence the simulated span and its monitor
+        // ticks) shrinks with the device concurrency
+        int dsum = 0;
+        if (s.device_model == GFQ_DEVMODEL_SCRIPTED) dsum = s.scripted_d;
+        else for (int d = 0; d < s.n_devices; d++) dsum += h->h_dcfg[s.device_cfg + d].d_max;
+        cost[i] = (double)n * (1.0 + nf / 32.0) * (s.policy == GFQ_POLICY_MQFQ ? 2.0 : 1.0) *
+                  (1.0 + 1.0 / (double)std::max(dsum, 1));
     }
     flows = foffs[n_sims]; recs = roffs[n_sims];
     Layout L{};
@@ -829,6 +866,22 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, smem));
         if (per_sm < 1) return set_err(GFQ_EINVAL, "gfq_prepare: kernel does not fit on an SM");
+        // then give the rest of the unified array back to L1: the read-only
+        // flow tables, per-flow arrival index and trace windows of an SM's
+        // simulations stay L1-resident instead of costing an L2 round trip
+        // on every dispatch
+        {
+            const double need = (double)per_sm * (double)(smem + 1024);
+            int pct = (int)ceil(100.0 * need / (double)h->smem_per_sm);
+            pct = std::min(100, std::max(pct, 1));
+            if (getenv("GFQ_CARVEOUT")) pct = atoi(getenv("GFQ_CARVEOUT"));
+            CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            int per_sm2 = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kfn, threads, smem));
+            if (per_sm2 < per_sm)                 // keep the occupancy
+                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared));
+        }
         int blocks = c.blocks > 0 ? c.blocks : per_sm * h->n_sm;
         cblocks[k] = std::max(1, std::min(blocks, (ccount[k] + per_cta - 1) / per_cta));
     }
@@ -851,7 +904,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         (rc = h->work.ensure(4 * NCLASS)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
         (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))) ||
         (gscr && (rc = h->gscratch.ensure(gscr))) ||
-        ((c.outputs & GFQ_WANT_RECORDS) && (rc = h->comp_pos.ensure(4 * std::max<int64_t>(recs, 1)))))
+        (rc = h->comp_pos.ensure(4 * std::max<int64_t>(recs, 1))))
         return rc;
     for (int id = 0; id < GFQ_OUT_COUNT_; id++) h->out_n[id] = 0;
     if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, (int64_t)GFQ_NCOUNTERS * n_sims)) ||

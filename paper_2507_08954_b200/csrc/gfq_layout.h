@@ -19,7 +19,7 @@ enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
 // per-device int fields
 enum { DV_OUT = 0, DV_EFFD, DV_HROK, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_INSTDIRTY, DV_INSTID,
        DV_ZAGE, DV_NSTATE,                                   // hot mutable state (registers
-       DV_WDICT_N = DV_NSTATE,                               //  in the 1-device build);
+       DV_SPARE0 = DV_NSTATE,                                //  in the 1-device build);
        DV_DMAX, DV_POOLMAX, DV_POOLON, DV_DYN,               //  DeviceConfig copy
        DV_NI = 16 };
 // per-device double fields: state, then a copy of the device's DeviceConfig
@@ -73,6 +73,8 @@ struct Layout {
     int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u64[ND][WMEMO], f64[ND][WMEMO]
     int32_t o_diag;                                      // u32[DG_N]
     int32_t o_newly;                                     // i32[NEWLY_CAP]
+    int32_t o_cst, o_csp, o_csm;                         // completion staging: f64[32], i32[32], i32[32]
+    int32_t o_rgt, o_rgf, o_mbar;                        // arrival window: f64[64], i32[64], 2 mbarriers
     int32_t o_cta;                                       // CtaCmd (CTA-per-simulation mode only)
     int32_t dev_bytes;
     // the fe part lives in shared memory in front of the device part, or (for
@@ -144,6 +146,13 @@ inline void layout_finish(Layout& L) {
     L.o_cnt = take(2 * 3 * ND * F);
     L.fe_bytes = o;
     o = 0;
+    auto take16 = [&](int32_t bytes) { o = (o + 15) & ~15; return take(bytes); };
+    if (L.cta) {                                 // CTA mode only (WarpSim::RING / CSTAGE)
+        L.o_rgt = take16(8 * 64); L.o_rgf = take16(4 * 64); L.o_mbar = take16(24);   // TMA targets, mbarriers + parity
+        L.o_cst = take(8 * 32); L.o_csp = take(4 * 32); L.o_csm = take(4 * 32);
+    } else {
+        L.o_rgt = L.o_rgf = L.o_mbar = L.o_cst = L.o_csp = L.o_csm = 0;
+    }
     L.o_dvi = take(4 * DV_NI * ND); L.o_dvd = take(8 * DD_ND * ND);
     L.o_smp_t = take(8 * ND * S); L.o_smp_u = take(8 * ND * S);
     L.o_run_i = take(4 * 4 * ND * R); L.o_run_d = take(8 * 2 * ND * R);
@@ -152,7 +161,8 @@ inline void layout_finish(Layout& L) {
     L.o_diag = take(4 * DG_N);
     L.o_newly = take(4 * NEWLY_CAP);
     L.o_cta = L.cta ? take((int32_t)sizeof(CtaCmd)) : 0;
-    L.dev_bytes = o;
+    L.dev_bytes = (o + 15) & ~15;
+    L.fe_bytes = (L.fe_bytes + 15) & ~15;                // keep every slice 16-byte aligned
     L.bytes = L.flows_global ? L.dev_bytes : L.fe_bytes + L.dev_bytes;
 }
 

@@ -56,6 +56,18 @@ namespace gfq {
 #endif
 #define FI __device__ __forceinline__
 typedef unsigned long long u64;
+// Latency-bound builds only (CTA mode: one event-loop warp per SM): the
+// arrival window in shared memory fed by TMA bulk copies, and the completion
+// stream staged in shared memory with a coalesced write-back.  The
+// warp-per-simulation builds run 16 event loops per SM, which hide the L2
+// latency these remove but not the instruction-cache footprint they add
+// (measured: each costs ~10% on C3).
+#ifndef GFQ_RING
+#define GFQ_RING 1
+#endif
+#ifndef GFQ_CSTAGE
+#define GFQ_CSTAGE 1
+#endif
 
 // ------------------------------------------------------------------------
 // warp primitives
@@ -132,6 +144,19 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 // and the audit / event logs; the others are one policy on a DeviceSet.
 enum { PB_GENERIC = 0, PB_MQFQ = 1, PB_FCFS = 2, PB_BATCH = 3, PB_SJF = 4 };
 
+// Once per warp slice at kernel start: the arrival window's two mbarriers
+// (see WarpSim::ring_start) and their phase-parity word.
+FI void ring_init(unsigned char* dev_base, const Layout& L, int lane) {
+    if (lane == 0) {
+        const uint32_t mb = (uint32_t)__cvta_generic_to_shared(dev_base + L.o_mbar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        *(uint32_t*)(dev_base + L.o_mbar + 16) = 0;
+    }
+    __syncwarp();
+}
+
 // CTA-mode scan kinds (the leader warp's command to the helper warps)
 enum { OP_EXIT = 0, OP_GVT, OP_REFRESH, OP_CAND, OP_BATCH, OP_SJF, OP_EVMIN };
 
@@ -154,6 +179,8 @@ FI void cta_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(
 template <int POL, bool ND1, bool CTA = false>
 struct WarpSim {
     static constexpr bool G = POL == PB_GENERIC;
+    static constexpr bool RING = CTA && GFQ_RING;
+    static constexpr bool CSTAGE = CTA && GFQ_CSTAGE;
     const Params& P;
     unsigned char* const sm;   // device part of this warp's state (shared memory)
     unsigned char* const fe;   // flow/event part (shared memory, or global scratch)
@@ -199,6 +226,11 @@ struct WarpSim {
     FI u64& WKEY(int d, int i) const { return ((u64*)(sm + P.L.o_wkey))[d * WMEMO + i]; }
     FI double& WVAL(int d, int i) const { return ((double*)(sm + P.L.o_wval))[d * WMEMO + i]; }
     FI int* NEWLY() const { return (int*)(sm + P.L.o_newly); }
+    FI double* CST() const { return (double*)(sm + P.L.o_cst); }      // completion staging
+    FI int* CSP() const { return (int*)(sm + P.L.o_csp); }
+    FI int* CSM() const { return (int*)(sm + P.L.o_csm); }
+    FI double* RGT() const { return (double*)(sm + P.L.o_rgt); }      // arrival window
+    FI int* RGF() const { return (int*)(sm + P.L.o_rgf); }
     FI uint16_t& CNT(int d, int kind, int f) const {   // kind: 0 gpu-warm, 1 host-warm, 2 running
         return ((uint16_t*)(fe + P.L.o_cnt))[(d * 3 + kind) * P.L.F + f];
     }
@@ -221,13 +253,87 @@ struct WarpSim {
 #define SJF (G ? policy == GFQ_POLICY_SJF : POL == PB_SJF)
     double T, alpha, dttl, period;
 
-    FI double arr(int i) const { return P.arrival[toff + i]; }
-    FI int flw(int i) const { return P.flow[toff + i]; }
-    FI double warm(int f) const { return P.warm[tb + f]; }
-    FI double cold(int f) const { return P.cold[tb + f]; }
-    FI double mem(int f) const { return P.mem[tb + f]; }
-    FI double share(int f) const { return P.share[tb + f]; }
-    FI double weight(int f) const { return P.weight[tb + f]; }
+    // read-only inputs through the non-coherent path (L1-resident: the flow
+    // tables of an SM's simulations and their trace windows are small)
+    FI double arr(int i) const { return __ldg(P.arrival + toff + i); }
+    FI int flw(int i) const { return __ldg(P.flow + toff + i); }
+    FI double warm(int f) const { return __ldg(P.warm + tb + f); }
+    FI double cold(int f) const { return __ldg(P.cold + tb + f); }
+    FI double mem(int f) const { return __ldg(P.mem + tb + f); }
+    FI double share(int f) const { return __ldg(P.share + tb + f); }
+    FI double weight(int f) const { return __ldg(P.weight + tb + f); }
+
+    // ---- arrival window: the trace streams through a 2 x 32-entry ring in
+    // shared memory, each 32-entry chunk (32-aligned global trace index)
+    // fetched by one TMA bulk copy (cp.async.bulk, mbarrier completion) a
+    // chunk ahead of the cursor.  The parity word (bit h = the phase parity to
+    // wait for on half h) sits in shared memory next to the mbarriers.
+    FI int ring_last() const { return (int)((toff + n - 1) >> 5); }   // n > 0
+    FI uint32_t mbar_addr(int h) const {
+        return (uint32_t)__cvta_generic_to_shared(sm + P.L.o_mbar + 8 * h);
+    }
+    FI void ring_issue(int c) {        // lane 0: fetch chunk c into half c & 1
+        const int h = c & 1;
+        const uint32_t mb = mbar_addr(h);
+        const uint32_t dt = (uint32_t)__cvta_generic_to_shared(RGT() + 32 * h);
+        const uint32_t df = (uint32_t)__cvta_generic_to_shared(RGF() + 32 * h);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(384) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];"
+                     ::"r"(dt), "l"(P.arrival + (int64_t)c * 32), "r"(mb) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
+                     ::"r"(df), "l"(P.flow + (int64_t)c * 32), "r"(mb) : "memory");
+    }
+    FI void ring_wait_chunk(int c) {   // every lane waits for chunk c
+        const int h = c & 1;
+        const uint32_t ph = *ring_ph_slot();
+        const uint32_t mb = mbar_addr(h), par = (ph >> h) & 1u;
+        uint32_t done = 0;
+        #pragma unroll 1
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(mb), "r"(par) : "memory");
+        __syncwarp();
+        if (lane == 0) *ring_ph_slot() = ph ^ (1u << h);
+        __syncwarp();
+    }
+    // The two mbarriers are initialised once per warp slice when the kernel
+    // starts (ring_init) and keep their phases across the simulations the
+    // warp runs; the parity bits live next to them between simulations.
+    FI uint32_t* ring_ph_slot() const { return (uint32_t*)(sm + P.L.o_mbar + 16); }
+    FI void ring_start() {
+        if (n <= 0) return;
+        const int c0 = (int)(toff >> 5);
+        if (lane == 0) {
+            ring_issue(c0);
+            if (c0 < ring_last()) ring_issue(c0 + 1);
+        }
+        __syncwarp();
+        ring_wait_chunk(c0);
+    }
+    // the cursor moved to trace position i: entering a new chunk waits for it
+    // (fetched one chunk ago) and fetches the next one into the other half,
+    // whose previous chunk has been fully consumed
+    FI void ring_enter(int i) {
+        const int64_t g = toff + i;
+        if ((g & 31) != 0) return;
+        const int c = (int)(g >> 5);
+        ring_wait_chunk(c);
+        if (c < ring_last()) {
+            if (lane == 0) ring_issue(c + 1);
+            __syncwarp();
+        }
+    }
+    // no bulk copy may outlive the simulation: the chunk after the last one
+    // entered (the cursor's, or the final entry's) is in flight unless it
+    // does not exist
+    FI void ring_drain() {
+        if (n > 0) {
+            const int c = (int)((toff + min(cursor, n - 1)) >> 5);
+            if (c < ring_last()) ring_wait_chunk(c + 1);
+        }
+    }
+    FI double ring_t(int i) const { return RGT()[(toff + i) & 63]; }
+    FI int ring_f(int i) const { return RGF()[(toff + i) & 63]; }
 
     // ---- uniform scalar state (registers)
     double now, gvt;
@@ -615,13 +721,13 @@ struct WarpSim {
         ust(CNT(d, 2, fn), (uint16_t)(CNT(d, 2, fn) + 1));
         if (!SCRIPTED) ust(DV(d, DV_INSTDIRTY), 1);
     }
-    FI bool run_remove(int d, int inv, double& duration, double& pure, int& st) {
+    FI bool run_remove(int d, int inv, double& duration, double& pure, int& st, int& fn) {
         int nr = DV(d, DV_NRUN);
         int ri = -1;
         #pragma unroll 1
         for (int r = 0; r < nr; r++) if (RI(d, r, 0) == inv) { ri = r; break; }
         if (ri < 0) { fail(GFQ_SIM_BAD_CONFIG); return false; }   // RuntimeError
-        int fn = RI(d, ri, 1);
+        fn = RI(d, ri, 1);
         st = RI(d, ri, 2); duration = RD(d, ri, 0); pure = RD(d, ri, 1);
         #pragma unroll 1
         for (int r = ri; r < nr - 1; r++) {
@@ -684,8 +790,8 @@ struct WarpSim {
     }
 
     // Device.complete, device.py:220-237
-    FI bool device_complete(int d, int inv, int fn, double& duration, double& pure, int& st) {
-        if (!run_remove(d, inv, duration, pure, st)) return false;
+    FI bool device_complete(int d, int inv, int& fn, double& duration, double& pure, int& st) {
+        if (!run_remove(d, inv, duration, pure, st, fn)) return false;
         ust(DV(d, DV_OUT), DV(d, DV_OUT) - 1);
         if (!DV(d, DV_POOLON)) return true;
         int np = DV(d, DV_NP);
@@ -721,12 +827,25 @@ struct WarpSim {
         int id = DV(d, DV_INSTID);
         if (DV(d, DV_INSTDIRTY)) {              // the running set changed since the last tick
             util = instantaneous_util(d);
-            int nd = DV(d, DV_WDICT_N);
+            // intern: open-addressed table of WDICT slots (id = slot + 1),
+            // empty slots hold an all-ones pattern (a NaN, never a utilization)
+            const u64 ub = (u64)__double_as_longlong(util);
+            int sl = (int)((((uint32_t)ub ^ (uint32_t)(ub >> 32)) * 0x9E3779B1u) >> 28);
+            if (sl >= WDICT) sl = 0;
             id = 0;
             #pragma unroll 1
-            for (int i = 0; i < nd; i++) if (WDICTV(d, i) == util) { id = i + 1; break; }
-            __syncwarp();
-            if (id == 0 && nd < WDICT) { WDICTV(d, nd) = util; DV(d, DV_WDICT_N) = nd + 1; id = nd + 1; }
+            for (int k = 0; k < WDICT; k++) {
+                const u64 v = (u64)__double_as_longlong(WDICTV(d, sl));
+                if (v == ub) { id = sl + 1; break; }
+                if (v == ~0ull) {
+                    __syncwarp();
+                    WDICTV(d, sl) = util;
+                    __syncwarp();
+                    id = sl + 1;
+                    break;
+                }
+                if (++sl == WDICT) sl = 0;
+            }
             DD(d, DD_INST) = util; DV(d, DV_INSTDIRTY) = 0; DV(d, DV_INSTID) = id;
             __syncwarp();
         }
@@ -753,7 +872,7 @@ struct WarpSim {
         u64 key = 0; int slot = 0;
         if (memo) {
             key = (code & ((1ull << (4 * ns)) - 1)) | ((u64)ns << 60);
-            slot = (int)((key * 0x9E3779B97F4A7C15ull) >> 60);
+            slot = (int)((((uint32_t)key ^ (uint32_t)(key >> 32)) * 0x9E3779B1u) >> 28);
         }
         const u64 lkey = (u64)__double_as_longlong(DD(d, DD_LKEY));
         if (memo && key == lkey) {                    // same window as the last tick
@@ -770,13 +889,18 @@ struct WarpSim {
             avg = ps_val(a) / (double)ns;
             if (memo) { __syncwarp(); WKEY(d, slot) = key; WVAL(d, slot) = avg; __syncwarp(); }
         }
-        int effd = DV(d, DV_EFFD);
-        const int dmax = DV(d, DV_DMAX);
-        const double thr = DD(d, DD_THR), inv = DD(d, DD_INVDMAX);
-        if (!DV(d, DV_DYN)) effd = dmax;
-        else if (avg > thr) effd = max(effd - 1, 1);
-        else if (avg < thr - inv) effd = min(effd + 1, dmax);
-        int hrok = !(avg + inv > thr);                                  // device.py:137-139
+        int effd = DV(d, DV_EFFD), hrok = DV(d, DV_HROK);
+        const bool dyn = DV(d, DV_DYN);
+        // a fixed D and an unchanged average leave effective_d and the
+        // headroom check as they were
+        if (dyn || __double_as_longlong(avg) != __double_as_longlong(UAVG(d))) {
+            const int dmax = DV(d, DV_DMAX);
+            const double thr = DD(d, DD_THR), inv = DD(d, DD_INVDMAX);
+            if (!dyn) effd = dmax;
+            else if (avg > thr) effd = max(effd - 1, 1);
+            else if (avg < thr - inv) effd = min(effd + 1, dmax);
+            hrok = !(avg + inv > thr);                                  // device.py:137-139
+        }
         __syncwarp();
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
         DV(d, DV_HROK) = hrok; DV(d, DV_ZAGE) = zage;
@@ -965,7 +1089,7 @@ struct WarpSim {
             // FlowQueue.pending.popleft()
             inv = head()[fn];
             int k = ph()[fn] + 1;
-            int nxt = k < pt()[fn] ? P.fpos[toff + foff[fn] + k] : -1;
+            int nxt = k < pt()[fn] ? __ldg(P.fpos + toff + __ldg(foff + fn) + k) : -1;
             int pe = pend()[fn] - 1, ninf = infl()[fn] + 1;
             double vt_before = vt()[fn];
             double nvt = vt_before;
@@ -1156,8 +1280,7 @@ struct WarpSim {
         }
     }
 
-    FI void on_arrival(int inv) {                         // engine.py:121-129
-        int fn = flw(inv);
+    FI void on_arrival(int inv, int fn) {                 // engine.py:121-129
         if (!SCRIPTED) {
             if (pt()[fn] - done()[fn] == 0) backlog_audit(fn, true);   // _backlog_change(+1)
             if (fst()[fn] & FL_MARKED) {                   // unmark_evictable on every device
@@ -1177,12 +1300,26 @@ struct WarpSim {
         if (!SCRIPTED && !tick_on) push(now + period, EV_TICK, 0);
     }
 
+    // Completion stream (InvocationRecords in completion order, read by the
+    // reducer and the fairness audit): staged 32 at a time in shared memory
+    // and written back by the whole warp, coalesced.
+    FI void comp_flush(int cnt) {
+        __syncwarp();
+        if (lane < cnt) {
+            const int64_t o = roff + ((n_comp - 1) & ~31) + lane;
+            P.comp_lat[o] = CST()[lane];
+            P.comp_pos[o] = CSP()[lane];
+            P.comp_meta[o] = CSM()[lane];
+        }
+        __syncwarp();
+    }
+
     FI void on_completion(int inv, int dev) {             // engine.py:131-153
-        int fn = flw(inv);
+        int fn = 0;
         double duration = 0.0, pure = 0.0; int st = 0;
         if (SCRIPTED) {
             s_out -= 1;
-            if (!run_remove(0, inv, duration, pure, st)) return;
+            if (!run_remove(0, inv, duration, pure, st, fn)) return;
             policy_on_completion(fn, duration);
         } else {
             if (!device_complete(dev, inv, fn, duration, pure, st)) return;
@@ -1190,15 +1327,20 @@ struct WarpSim {
         }
         int k = n_comp++;
         if (lane == 0) {
-            int64_t o = roff + k;
-            P.comp_lat[o] = now - arr(inv);
-            P.comp_meta[o] = fn | ((st == GFQ_COLD) ? (int)0x80000000 : 0);
+            const int cm = fn | ((st == GFQ_COLD) ? (int)0x80000000 : 0);
+            if (CSTAGE) {
+                CST()[k & 31] = now;        // latency = now - arrival, taken by the reducer
+                CSP()[k & 31] = inv;
+                CSM()[k & 31] = cm;
+            } else {
+                P.comp_lat[roff + k] = now; P.comp_pos[roff + k] = inv; P.comp_meta[roff + k] = cm;
+            }
             if (P.outputs & GFQ_WANT_RECORDS) {
                 P.rec_complete[roff + inv] = now;
                 P.rec_order[roff + inv] = k;
-                P.comp_pos[o] = inv;
             }
         }
+        if (CSTAGE && (k & 31) == 31) comp_flush(32);
         if (!SCRIPTED && pt()[fn] - done()[fn] == 0) {     // _backlog_change(-1)
             backlog_audit(fn, false);
             if (MQFQ) push(now + ttl(fn), EV_EXPIRY, (uint32_t)fn);
@@ -1262,7 +1404,8 @@ struct WarpSim {
         long long me = sim->max_events > 0 ? sim->max_events : 64ll * ((long long)n + 1024);
         const int max_events = (int)min(me, 0x7fffffffll);
         const double INF = __longlong_as_double(0x7ff0000000000000ll);
-        double t_arr = n > 0 ? arr(0) : INF;
+        if (RING) ring_start();
+        double t_arr = n > 0 ? (RING ? ring_t(0) : arr(0)) : INF;
         const bool early = P.early_exit && !(G && (P.outputs & GFQ_WANT_EVENTS));
         #pragma unroll 1
         for (;;) {
@@ -1286,9 +1429,15 @@ struct WarpSim {
             bool dr = true;
             if (kind == EV_ARRIVAL) {
                 int inv = cursor++;
-                t_arr = cursor < n ? arr(cursor) : INF;
+                const int fn = RING ? ring_f(inv) : flw(inv);
+                if (cursor < n) {
+                    if (RING) { ring_enter(cursor); t_arr = ring_t(cursor); }
+                    else t_arr = arr(cursor);
+                } else {
+                    t_arr = INF;
+                }
                 log_event(t, EV_ARRIVAL, inv);
-                on_arrival(inv);
+                on_arrival(inv, fn);
             } else if (kind == EV_TICK) {
                 // A run of ticks: while the drain after a tick is provably quiet
                 // (one counted dispatch() call, no state change) and the next
@@ -1332,6 +1481,8 @@ struct WarpSim {
             if (UNLIKELY(status)) break;
             if (!SCRIPTED) swap_out_inactive();
         }
+        if (RING) ring_drain();
+        if (CSTAGE && (n_comp & 31)) comp_flush(n_comp & 31);
     }
 };
 
