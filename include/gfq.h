@@ -219,6 +219,26 @@ int  gfq_destroy(gfq_handle* h);
 int  gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
                        const int64_t* off, const int32_t* n_flows, int32_t n_traces);
 
+/* Synthetic traces generated on the GPU, in place of gfq_upload_traces: the
+ * reference's gen_zipf (workload.py:82-111) for n_traces traces at once,
+ * bit-identical to it (numpy 2.3 SeedSequence.spawn + PCG64 + the
+ * exponential ziggurat + round(t, 6) + sort by (t, name)).  Per trace t:
+ * n_functions[t] functions in the caller's order (the names= order of
+ * gen_zipf); rates[] = zipf_rates(...) for them (concatenated per trace);
+ * name_rank[] = each function's position in the sorted name list;
+ * duration_s[t]; seed[t] (< 2^64).  Outputs (optional): touched[] (1 if the
+ * function arrived at least once, same layout as rates) and
+ * trace_off[n_traces + 1].  The resident traces are replaced exactly as by
+ * gfq_upload_traces, with flow ids = rank among the touched names. */
+int  gfq_generate_traces(gfq_handle* h, int32_t n_traces, const int32_t* n_functions,
+                         const double* rates, const int32_t* name_rank,
+                         const double* duration_s, const uint64_t* seed,
+                         uint8_t* touched, int64_t* trace_off);
+
+/* Copy the resident traces (uploaded or generated) back to the host:
+ * arrival[total] and flow[total], total = trace_off[n_traces]. */
+int  gfq_download_traces(gfq_handle* h, double* arrival, int32_t* flow, int64_t total);
+
 /* Flow tables: FunctionProfile fields (core.py:30-51) for one trace's flows,
  * in flow-rank order, plus the effective scheduler weight (weight_of,
  * mqfq.py:88-92) and a histogram row id.  off has n_tabs+1 entries.      */

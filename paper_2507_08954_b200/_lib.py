@@ -38,6 +38,10 @@ _SIGS = {
     "gfq_synchronize": (C.c_int, [C.c_void_p]),
     "gfq_last_kernel_ms": (C.c_int, [C.c_void_p, _P(C.c_float), _P(C.c_float)]),
     "gfq_batch_info": (C.c_int, [C.c_void_p, _P(C.c_int32), C.c_int32]),
+    "gfq_generate_traces": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_int32), _P(C.c_double),
+                                      _P(C.c_int32), _P(C.c_double), _P(C.c_uint64),
+                                      _P(C.c_uint8), _P(C.c_int64)]),
+    "gfq_download_traces": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_int32), C.c_int64]),
     "gfq_kernel_times": (C.c_int, [C.c_void_p, _P(C.c_float), _P(C.c_float), C.c_int32,
                                    _P(C.c_int32)]),
     "gfq_output_info": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_int64), _P(C.c_int32)]),

@@ -27,8 +27,11 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include "sim_warp.cuh"
 #include "fairness.cuh"
+#include "tracegen.cuh"
 
 #ifndef GFQ_TIMELINE
 #define GFQ_TIMELINE 0      // diagnostic build: per-simulation start/end time and SM in the counters
@@ -485,6 +488,10 @@ struct DBuf {
         return GFQ_OK;
     }
     void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
     template <class T> T* as() const { return (T*)p; }
 };
 
@@ -588,6 +595,9 @@ int gfq_destroy(gfq_handle* h) {
     return GFQ_OK;
 }
 
+static int index_traces(gfq_handle* h, const int64_t* off, const int32_t* n_flows, int32_t n_traces,
+                        const std::vector<int64_t>& foff_off, int32_t max_nf);
+
 int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
                       const int64_t* off, const int32_t* n_flows, int32_t n_traces) {
     if (!h || n_traces < 0 || (n_traces > 0 && (!off || !n_flows)))
@@ -630,6 +640,13 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
     }
     CK(cudaMemcpy(h->trace_off.p, off, 8 * (n_traces + 1), cudaMemcpyHostToDevice));
     if (n_traces) CK(cudaMemcpy(h->trace_nf.p, n_flows, 4 * n_traces, cudaMemcpyHostToDevice));
+    return index_traces(h, off, n_flows, n_traces, foff_off, max_nf);
+}
+
+// Per-flow arrival index of the resident traces (k_trace_index) and the
+// host-side trace table; arrival / flow / trace_off / trace_nf are on the device.
+static int index_traces(gfq_handle* h, const int64_t* off, const int32_t* n_flows, int32_t n_traces,
+                        const std::vector<int64_t>& foff_off, int32_t max_nf) {
     CK(cudaMemcpy(h->foff_off.p, foff_off.data(), 8 * (n_traces + 1), cudaMemcpyHostToDevice));
     if (n_traces) {
         size_t sm = 4 * ((size_t)max_nf + 1);
@@ -644,6 +661,134 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
     h->h_trace_nf.assign(n_flows, n_flows + n_traces);
     h->n_traces = n_traces;
     h->prepared = false;
+    return GFQ_OK;
+}
+
+int gfq_generate_traces(gfq_handle* h, int32_t n_traces, const int32_t* n_functions,
+                        const double* rates, const int32_t* name_rank, const double* duration_s,
+                        const uint64_t* seed, uint8_t* touched, int64_t* trace_off_out) {
+    if (!h || n_traces < 0 || (n_traces > 0 && (!n_functions || !rates || !name_rank || !duration_s || !seed)))
+        return set_err(GFQ_EINVAL, "gfq_generate_traces: bad arguments");
+    CK(cudaSetDevice(h->device));
+    // streams of a trace in name order: stream (t, j) is the function whose
+    // name rank is j, so a stable sort by time gives (t, name) order
+    std::vector<int64_t> fn_off(n_traces + 1, 0);
+    for (int t = 0; t < n_traces; t++) {
+        if (n_functions[t] < 1 || n_functions[t] > 0xffff)
+            return set_err(GFQ_EINVAL, "n_functions must be in [1, 65535]");
+        if (!isfinite(duration_s[t]))        // (a negative duration gives an empty trace, as in gen_zipf)
+            return set_err(GFQ_EINVAL, "gfq_generate_traces: duration must be finite");
+        fn_off[t + 1] = fn_off[t] + n_functions[t];
+    }
+    const int64_t nfn = fn_off[n_traces];
+    std::vector<int32_t> st(nfn), sf(nfn), sr(nfn);
+    for (int t = 0; t < n_traces; t++) {
+        const int64_t a = fn_off[t];
+        const int n = n_functions[t];
+        std::vector<int32_t> inv(n, -1);
+        for (int k = 0; k < n; k++) {
+            const int r = name_rank[a + k];
+            if (r < 0 || r >= n || inv[r] >= 0) return set_err(GFQ_EINVAL, "gfq_generate_traces: name_rank is not a permutation");
+            if (!(rates[a + k] > 0) || !isfinite(rates[a + k])) return set_err(GFQ_EINVAL, "total_rate_rps must be > 0");
+            inv[r] = k;
+        }
+        for (int j = 0; j < n; j++) { st[a + j] = t; sf[a + j] = inv[j]; sr[a + j] = j; }
+    }
+    DBuf d_st, d_sf, d_sr, d_fo, d_rt, d_du, d_sd, d_cnt, d_oo, d_k0, d_k1, d_v0, d_v1, d_tmp, d_map, d_tch;
+    int rc;
+    const size_t ns = (size_t)std::max<int64_t>(nfn, 1);
+    if ((rc = d_st.ensure(4 * ns)) || (rc = d_sf.ensure(4 * ns)) || (rc = d_sr.ensure(4 * ns)) ||
+        (rc = d_fo.ensure(8 * (n_traces + 1))) || (rc = d_rt.ensure(8 * ns)) ||
+        (rc = d_du.ensure(8 * std::max(n_traces, 1))) || (rc = d_sd.ensure(8 * std::max(n_traces, 1))) ||
+        (rc = d_cnt.ensure(8 * ns)) || (rc = d_oo.ensure(8 * ns)) || (rc = d_map.ensure(4 * ns)) ||
+        (rc = d_tch.ensure(ns)))
+        return rc;
+    if (nfn) {
+        CK(cudaMemcpy(d_st.p, st.data(), 4 * nfn, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_sf.p, sf.data(), 4 * nfn, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_sr.p, sr.data(), 4 * nfn, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_rt.p, rates, 8 * nfn, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(d_fo.p, fn_off.data(), 8 * (n_traces + 1), cudaMemcpyHostToDevice));
+    if (n_traces) {
+        CK(cudaMemcpy(d_du.p, duration_s, 8 * n_traces, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_sd.p, seed, 8 * n_traces, cudaMemcpyHostToDevice));
+    }
+    GenParams g{};
+    g.n_streams = (int32_t)nfn;
+    g.stream_trace = d_st.as<int32_t>(); g.stream_fn = d_sf.as<int32_t>(); g.stream_rank = d_sr.as<int32_t>();
+    g.fn_off = d_fo.as<int64_t>(); g.rates = d_rt.as<double>(); g.duration = d_du.as<double>();
+    g.seed = d_sd.as<unsigned long long>(); g.count = d_cnt.as<int64_t>(); g.out_off = d_oo.as<int64_t>();
+    const int gb = (int)((nfn + 127) / 128);
+    // pass 1: arrivals per stream
+    if (nfn) { k_gen_streams<<<gb, 128>>>(g, 0); CK(cudaGetLastError()); }
+    std::vector<int64_t> cnt(nfn), oo(nfn), toff(n_traces + 1, 0);
+    if (nfn) CK(cudaMemcpy(cnt.data(), d_cnt.p, 8 * nfn, cudaMemcpyDeviceToHost));
+    int64_t total = 0;
+    for (int t = 0; t < n_traces; t++) {
+        for (int64_t i = fn_off[t]; i < fn_off[t + 1]; i++) { oo[i] = total; total += cnt[i]; }
+        toff[t + 1] = total;
+        if (toff[t + 1] - toff[t] >= (1 << 27)) return set_err(GFQ_EINVAL, "gfq_generate_traces: trace longer than 2^27 arrivals");
+    }
+    const size_t na = (size_t)std::max<int64_t>(total, 1);
+    if ((rc = d_k0.ensure(8 * na)) || (rc = d_k1.ensure(8 * na)) || (rc = d_v0.ensure(4 * na)) || (rc = d_v1.ensure(4 * na)))
+        return rc;
+    if (nfn) CK(cudaMemcpy(d_oo.p, oo.data(), 8 * nfn, cudaMemcpyHostToDevice));
+    g.key = d_k0.as<unsigned long long>(); g.val = d_v0.as<int32_t>();
+    // pass 2: arrival times (rounded) + name ranks, streams in name order
+    if (nfn) { k_gen_streams<<<gb, 128>>>(g, 1); CK(cudaGetLastError()); }
+    // the engine's trace buffers (padded to whole 32-entry chunks, see upload)
+    const int64_t padded = ((total + 31) & ~(int64_t)31) + 32;
+    if ((rc = h->arrival.ensure(8 * padded)) || (rc = h->flow.ensure(4 * padded)) ||
+        (rc = h->fpos.ensure(4 * std::max<int64_t>(total, 1))) || (rc = h->trace_off.ensure(8 * (n_traces + 1))) ||
+        (rc = h->trace_nf.ensure(4 * std::max(n_traces, 1))))
+        return rc;
+    CK(cudaMemcpy(h->trace_off.p, toff.data(), 8 * (n_traces + 1), cudaMemcpyHostToDevice));
+    if (total) {
+        // stable sort of each trace by time (the fp64 bit pattern of t >= 0)
+        size_t tmp = 0;
+        CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, d_k0.as<unsigned long long>(), d_k1.as<unsigned long long>(),
+                                                    d_v0.as<int32_t>(), d_v1.as<int32_t>(), (int)total, n_traces,
+                                                    h->trace_off.as<int64_t>(), h->trace_off.as<int64_t>() + 1));
+        if ((rc = d_tmp.ensure(tmp))) return rc;
+        CK(cub::DeviceSegmentedRadixSort::SortPairs(d_tmp.p, tmp, d_k0.as<unsigned long long>(), d_k1.as<unsigned long long>(),
+                                                    d_v0.as<int32_t>(), d_v1.as<int32_t>(), (int)total, n_traces,
+                                                    h->trace_off.as<int64_t>(), h->trace_off.as<int64_t>() + 1));
+    }
+    if (n_traces) {
+        k_gen_flows<<<n_traces, 256>>>(d_k1.as<unsigned long long>(), d_v1.as<int32_t>(), h->trace_off.as<int64_t>(),
+                                       d_fo.as<int64_t>(), d_map.as<int32_t>(), h->arrival.as<double>(),
+                                       h->flow.as<int32_t>(), h->trace_nf.as<int32_t>(), d_tch.as<uint8_t>());
+        CK(cudaGetLastError());
+    }
+    std::vector<int32_t> nfl(std::max(n_traces, 1));
+    std::vector<uint8_t> tch(ns);
+    if (n_traces) CK(cudaMemcpy(nfl.data(), h->trace_nf.p, 4 * n_traces, cudaMemcpyDeviceToHost));
+    if (nfn) CK(cudaMemcpy(tch.data(), d_tch.p, nfn, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> foff_off(n_traces + 1, 0);
+    int32_t max_nf = 1;
+    for (int t = 0; t < n_traces; t++) {
+        foff_off[t + 1] = foff_off[t] + nfl[t] + 1;
+        max_nf = std::max(max_nf, nfl[t]);
+        if (touched)                          // back to the caller's function order
+            for (int64_t k = fn_off[t]; k < fn_off[t + 1]; k++) touched[k] = tch[fn_off[t] + name_rank[k]];
+    }
+    if ((rc = h->foff_off.ensure(8 * (n_traces + 1))) || (rc = h->foff.ensure(4 * std::max<int64_t>(foff_off[n_traces], 1))))
+        return rc;
+    if (trace_off_out) memcpy(trace_off_out, toff.data(), 8 * (n_traces + 1));
+    rc = index_traces(h, toff.data(), nfl.data(), n_traces, foff_off, max_nf);
+    for (DBuf* b : {&d_st, &d_sf, &d_sr, &d_fo, &d_rt, &d_du, &d_sd, &d_cnt, &d_oo, &d_k0, &d_k1, &d_v0, &d_v1, &d_tmp, &d_map, &d_tch})
+        b->release();
+    return rc;
+}
+
+int gfq_download_traces(gfq_handle* h, double* arrival, int32_t* flow, int64_t total) {
+    if (!h || total < 0) return set_err(GFQ_EINVAL, "gfq_download_traces: bad arguments");
+    const int64_t have = h->h_trace_off.empty() ? 0 : h->h_trace_off.back();
+    if (total != have) return set_err(GFQ_EINVAL, "gfq_download_traces: total does not match the resident traces");
+    CK(cudaSetDevice(h->device));
+    if (total && arrival) CK(cudaMemcpy(arrival, h->arrival.p, 8 * total, cudaMemcpyDeviceToHost));
+    if (total && flow) CK(cudaMemcpy(flow, h->flow.p, 4 * total, cudaMemcpyDeviceToHost));
     return GFQ_OK;
 }
 

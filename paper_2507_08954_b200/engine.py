@@ -115,6 +115,61 @@ class Engine:
         check(self._L.gfq_upload_traces(self._h, _ptr(arrival, C.c_double), _ptr(flow, C.c_int32),
                                         _ptr(off, C.c_int64), _ptr(nf, C.c_int32), len(traces)))
 
+    def generate_traces(self, specs) -> list[PackedTrace]:
+        """GPU gen_zipf (workload.py:82-111) for many traces, made resident as
+        by upload_traces.  specs: (n_functions, zipf_s, total_rate_rps,
+        duration_s, seed[, names]) tuples; names default to
+        default_profiles(n_functions).  Returns one PackedTrace per spec
+        (names = the touched functions in sorted order; arrays fetched from
+        the device)."""
+        from .workload import default_profiles, zipf_rates
+        nfs, rates, ranks, durs, seeds, names_all = [], [], [], [], [], []
+        for spec in specs:
+            n, s_, rate, dur, seed = spec[:5]
+            names = list(spec[5]) if len(spec) > 5 and spec[5] is not None else None
+            if n < 1:
+                raise ValueError("n_functions must be >= 1")
+            if rate <= 0:
+                raise ValueError("total_rate_rps must be > 0")
+            if names is None:
+                names = list(default_profiles(n))
+            if len(names) != n:
+                raise ValueError("names must match n_functions")
+            if not 0 <= int(seed) < 2 ** 64:
+                raise ValueError("seed must be in [0, 2**64)")
+            rates.extend(zipf_rates(n, s_, rate))
+            order = sorted(range(n), key=lambda k: names[k])
+            rk = [0] * n
+            for j, k in enumerate(order):
+                rk[k] = j
+            ranks.extend(rk)
+            nfs.append(n); durs.append(float(dur)); seeds.append(int(seed)); names_all.append(names)
+        nt = len(nfs)
+        nf_a = np.asarray(nfs, dtype=np.int32)
+        rt_a = np.asarray(rates, dtype=np.float64)
+        rk_a = np.asarray(ranks, dtype=np.int32)
+        du_a = np.asarray(durs, dtype=np.float64)
+        sd_a = np.asarray(seeds, dtype=np.uint64)
+        touched = np.zeros(max(len(rates), 1), dtype=np.uint8)
+        toff = np.zeros(nt + 1, dtype=np.int64)
+        check(self._L.gfq_generate_traces(self._h, nt, _ptr(nf_a, C.c_int32), _ptr(rt_a, C.c_double),
+                                          _ptr(rk_a, C.c_int32), _ptr(du_a, C.c_double),
+                                          _ptr(sd_a, C.c_uint64), _ptr(touched, C.c_uint8),
+                                          _ptr(toff, C.c_int64)))
+        total = int(toff[-1])
+        arrival = np.zeros(max(total, 1), dtype=np.float64)
+        flow = np.zeros(max(total, 1), dtype=np.int32)
+        check(self._L.gfq_download_traces(self._h, _ptr(arrival, C.c_double), _ptr(flow, C.c_int32),
+                                          total))
+        out, a = [], 0
+        for t in range(nt):
+            n = nfs[t]
+            tn = sorted(nm for nm, hit in zip(names_all[t], touched[a:a + n]) if hit)
+            a += n
+            lo, hi = int(toff[t]), int(toff[t + 1])
+            out.append(PackedTrace(tn, arrival[lo:hi].copy(), flow[lo:hi].copy()))
+        return out
+
     def upload_trace_arrays(self, arrival, flow, off, n_flows) -> None:
         """Pre-packed CSR arrays (e.g. pinned host buffers), no host copy."""
         check(self._L.gfq_upload_traces(self._h, _ptr(arrival, C.c_double), _ptr(flow, C.c_int32),
