@@ -238,8 +238,11 @@ def run_gfq(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    w = sweep.build(args.workload, rank, **({"n_seeds": args.seeds} if args.seeds else {}))
     eng = Engine(local)
+    # the sweep's traces come from the GPU trace generator (gfq_generate_traces,
+    # bit-identical to gen_zipf); the arrays are also kept on the host for the
+    # e2e leg's uploads and the CPU baseline
+    w = sweep.build(args.workload, rank, engine=eng, **({"n_seeds": args.seeds} if args.seeds else {}))
     w.upload(eng)
     outputs = _abi.WANT_STATS | _abi.WANT_HIST
     kw = dict(hist_groups=w.groups, hist_rows=w.hist_rows, hist_bins=sweep.HIST_BINS,

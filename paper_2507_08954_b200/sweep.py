@@ -57,13 +57,22 @@ class Workload:
         return arr
 
 
-def _traces(n_fn, s, rates_seeds, duration):
+def gen_traces(n_fn, s, rates_seeds, duration, profiles=None, engine=None) -> list[PackedTrace]:
+    """gen_zipf + pack_trace for each (rate, seed): on the GPU when an engine
+    is given (gfq_generate_traces, bit-identical), else on the host."""
+    profiles = profiles or default_profiles(n_fn)
+    if engine is not None:
+        return engine.generate_traces([(n_fn, s, rate, duration, seed, list(profiles))
+                                       for rate, seed in rates_seeds])
+    return [pack_trace(gen_zipf(n_fn, s, rate, duration, seed, names=list(profiles)).entries,
+                       profiles) for rate, seed in rates_seeds]
+
+
+def _traces(n_fn, s, rates_seeds, duration, engine=None):
     profiles = default_profiles(n_fn)
     order = {nm: i for i, nm in enumerate(profiles)}
     traces, tabs = [], []
-    for rate, seed in rates_seeds:
-        tr = gen_zipf(n_fn, s, rate, duration, seed)
-        pt = pack_trace(tr.entries, profiles)
+    for pt in gen_traces(n_fn, s, rates_seeds, duration, profiles, engine):
         traces.append(pt)
         # histogram row = the function's identity (profile index), not its
         # per-trace rank, so rows line up across traces and GPUs
@@ -71,9 +80,9 @@ def _traces(n_fn, s, rates_seeds, duration):
     return traces, tabs
 
 
-def c3(seed_base: int = 1, n_seeds: int = 16, duration: float = 600.0) -> Workload:
+def c3(seed_base: int = 1, n_seeds: int = 16, duration: float = 600.0, engine=None) -> Workload:
     seeds = list(range(seed_base, seed_base + n_seeds))
-    traces, tabs = _traces(100, 1.5, [(C3_RATE, s) for s in seeds], duration)
+    traces, tabs = _traces(100, 1.5, [(C3_RATE, s) for s in seeds], duration, engine)
     dcfgs = [DeviceConfig(d_max=d) for d in C3_D]
     sims = []
     for ti, t in enumerate(C3_T):
@@ -92,9 +101,9 @@ def c3(seed_base: int = 1, n_seeds: int = 16, duration: float = 600.0) -> Worklo
 
 
 def c2(seed_base: int = 1, n_seeds: int = 456, duration: float = 600.0,
-       policies=("mqfq", "fcfs", "batch")) -> Workload:
+       policies=("mqfq", "fcfs", "batch"), engine=None) -> Workload:
     rs = [(r, s) for s in range(seed_base, seed_base + n_seeds) for r in TABLE3_RPS]
-    traces, tabs = _traces(200, 1.5, rs, duration)
+    traces, tabs = _traces(200, 1.5, rs, duration, engine)
     dcfgs = [DeviceConfig()]
     sims = []
     cfg = SchedulerConfig()
@@ -112,7 +121,7 @@ C4_MEM_MB = [256.0, 512.0, 1024.0, 1500.0, 3000.0]
 
 
 def c4(seed_base: int = 1, n_seeds: int = 4, duration: float = 1800.0, rate: float = 2.0,
-       policies=("mqfq", "fcfs")) -> Workload:
+       policies=("mqfq", "fcfs"), engine=None) -> Workload:
     """BASELINE C4 (configs[3]): 4096 functions per simulation (Zipf 0.5, ~2.1k
     touched in 1800 s at 2 rps), heterogeneous memory (mem_mb by rank mod 5),
     16 GB device, D=4, container pool 32 or 256 -> cold starts, host-warm
@@ -127,8 +136,7 @@ def c4(seed_base: int = 1, n_seeds: int = 4, duration: float = 1800.0, rate: flo
     order = {nm: i for i, nm in enumerate(profiles)}
     traces, tabs = [], []
     seeds = list(range(seed_base, seed_base + n_seeds))
-    for seed in seeds:
-        pt = pack_trace(gen_zipf(n_fn, 0.5, rate, duration, seed).entries, profiles)
+    for pt in gen_traces(n_fn, 0.5, [(rate, sd) for sd in seeds], duration, profiles, engine):
         traces.append(pt)
         tabs.append(flow_table(pt.names, profiles, None, [order[nm] for nm in pt.names]))
     dcfgs = [DeviceConfig(d_max=4, pool_max_containers=pm) for pm in (32, 256)]
@@ -154,7 +162,7 @@ C5_SHARE = [0.2, 0.38, 0.5]
 C5_RHO = [0.7, 0.9, 1.0, 1.1]
 
 
-def c5(seed_base: int = 1, n_traces: int = 1563, duration: float = 600.0) -> Workload:
+def c5(seed_base: int = 1, n_traces: int = 1563, duration: float = 600.0, engine=None) -> Workload:
     """BASELINE C5 (configs[4]) per GPU: the 1M-simulation sensitivity sweep
     is 8 x ~125k.  Every trace (F=100 functions, heterogeneous memory /
     compute share / weight by rank, load rho in {0.7,0.9,1.0,1.1}) runs 80
@@ -171,9 +179,8 @@ def c5(seed_base: int = 1, n_traces: int = 1563, duration: float = 600.0) -> Wor
     tot = sum(shares)
     mean_exec = sum(sh / tot * p.warm_exec_s for sh, p in zip(shares, profiles.values()))
     traces, tabs = [], []
-    for j in range(n_traces):
-        rate = C5_RHO[j % 4] * 1.8 / mean_exec
-        pt = pack_trace(gen_zipf(n_fn, 1.5, rate, duration, seed_base + j).entries, profiles)
+    rs = [(C5_RHO[j % 4] * 1.8 / mean_exec, seed_base + j) for j in range(n_traces)]
+    for pt in gen_traces(n_fn, 1.5, rs, duration, profiles, engine):
         traces.append(pt)
         tabs.append(flow_table(pt.names, profiles, None, [order[nm] for nm in pt.names]))
     dcfgs = [DeviceConfig(d_max=d) for d in C5_D] + \
@@ -198,20 +205,21 @@ def c5(seed_base: int = 1, n_traces: int = 1563, duration: float = 600.0) -> Wor
                               "duration_s": duration, "sims": len(sims)})
 
 
-def build(name: str, rank: int = 0, **kw) -> Workload:
-    """Weak-scaling shard for `rank`: a disjoint block of seeds per GPU."""
+def build(name: str, rank: int = 0, engine=None, **kw) -> Workload:
+    """Weak-scaling shard for `rank`: a disjoint block of seeds per GPU.
+    With an engine the traces are generated on its GPU."""
     if name == "c3":
         n = kw.get("n_seeds", 16)
-        return c3(seed_base=1 + rank * n, n_seeds=n)
+        return c3(seed_base=1 + rank * n, n_seeds=n, engine=engine)
     if name == "c2":
         n = kw.get("n_seeds", 456)
-        return c2(seed_base=1 + rank * n, n_seeds=n)
+        return c2(seed_base=1 + rank * n, n_seeds=n, engine=engine)
     if name == "c4":
         n = kw.get("n_seeds", 37)          # 37 seeds x 2 pools x 2 policies = 148 sims, 1 per SM
-        return c4(seed_base=1 + rank * n, n_seeds=n)
+        return c4(seed_base=1 + rank * n, n_seeds=n, engine=engine)
     if name == "c5":
         n = kw.get("n_seeds", 1563)
-        return c5(seed_base=1 + rank * n, n_traces=n)
+        return c5(seed_base=1 + rank * n, n_traces=n, engine=engine)
     raise ValueError(f"unknown workload {name}")
 
 
