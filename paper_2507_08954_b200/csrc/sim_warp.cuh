@@ -465,6 +465,7 @@ struct WarpSim {
 
     FI void fail(int st) { if (!status) status = st; }
 #define UNLIKELY(x) __builtin_expect(!!(x), 0)
+#define LIKELY(x) __builtin_expect(!!(x), 1)
     FI double ttl(int f) const {                          // FlowQueue.ttl, core.py:140-152
         if (alpha == 0.0) return 0.0;
         if (pt()[f] >= 2) return alpha * iat()[f];       // iat.count = arrivals - 1
@@ -599,7 +600,7 @@ struct WarpSim {
         if (CNT(d, 0, fn) > 0) return true;               // idle GPU_WARM exists
         double needed = mem(fn);
         double free_mb = DD(d, DD_MEMCAP) - resident_mb(d);
-        if (free_mb >= needed) return true;
+        if (LIKELY(free_mb >= needed)) return true;
         int np = DV(d, DV_NP);
         int nsw = 0;
         #pragma unroll 1
@@ -772,7 +773,7 @@ struct WarpSim {
         #pragma unroll 1
         for (;;) {
             int np = DV(d, DV_NP), nr = DV(d, DV_NRUN);
-            if (!(np + nr > cap && np > 0)) break;
+            if (LIKELY(!(np + nr > cap && np > 0))) break;
             unsigned bk01 = 0xffffffffu; u64 bk2 = ~0ull; int bi = 0x7fffffff;
             #pragma unroll 1
             for (int i = lane; i < np; i += 32) {
@@ -877,7 +878,7 @@ struct WarpSim {
         const u64 lkey = (u64)__double_as_longlong(DD(d, DD_LKEY));
         if (memo && key == lkey) {                    // same window as the last tick
             avg = UAVG(d);
-        } else if (memo && WKEY(d, slot) == key) {
+        } else if (LIKELY(memo && WKEY(d, slot) == key)) {
             avg = WVAL(d, slot);
             diag(DG_WHIT);
         } else {
@@ -922,7 +923,7 @@ struct WarpSim {
             gmin = cta_scan(OP_GVT).k;
             gmin_ok = true;
         }
-        if (!gmin_ok) {
+        if (UNLIKELY(!gmin_ok)) {
             diag(DG_GSCAN);
             u64 bk = ~0ull;
             #pragma unroll 1
@@ -949,7 +950,7 @@ struct WarpSim {
     // restricted to what is observable: idle queues whose keep-alive expired
     // become INACTIVE (and are queued for swap-out).
     FI void refresh_states() {
-        if (now < idle_lb) return;
+        if (LIKELY(now < idle_lb)) return;
         diag(DG_RSCAN);
         if (cta_on(nf)) {
             CtaCmd* c = cmd();
@@ -1121,7 +1122,7 @@ struct WarpSim {
         int p0 = pt()[fn], pe = pend()[fn], d0 = done()[fn];
         double v = vt()[fn], le = lex()[fn], im = iat()[fn];
         int hd = head()[fn];
-        if (!(s & FL_CREATED)) {                          // queue_for, mqfq.py:94-99
+        if (UNLIKELY(!(s & FL_CREATED))) {                // queue_for, mqfq.py:94-99
             s = FL_CREATED | FL_INACTIVE;
             v = 0.0;
             le = MQFQ ? now : 0.0;
@@ -1181,7 +1182,7 @@ struct WarpSim {
 
     // _swap_out_inactive, engine.py:199-203 (+ Device.swap_out / mark_evictable)
     FI void swap_out_inactive() {
-        if (!any_newly) return;
+        if (LIKELY(!any_newly)) return;
         any_newly = false;
         #pragma unroll 1
         for (int d = 0; d < NDEV(); d++) {
@@ -1283,7 +1284,7 @@ struct WarpSim {
     FI void on_arrival(int inv, int fn) {                 // engine.py:121-129
         if (!SCRIPTED) {
             if (pt()[fn] - done()[fn] == 0) backlog_audit(fn, true);   // _backlog_change(+1)
-            if (fst()[fn] & FL_MARKED) {                   // unmark_evictable on every device
+            if (UNLIKELY(fst()[fn] & FL_MARKED)) {         // unmark_evictable on every device
                 #pragma unroll 1
                 for (int d = 0; d < NDEV(); d++) {
                     int np = DV(d, DV_NP);
