@@ -533,6 +533,10 @@ struct gfq_handle {
     int32_t out_b[GFQ_OUT_COUNT_] = {0};
     DBuf comp_lat, comp_meta, comp_pos, gscratch, fscratch;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    // kernel classes run concurrently on side streams (fork/join on the
+    // caller's stream), so one class's tail overlaps the next class's start
+    cudaStream_t side[8] = {};
+    cudaEvent_t fork = nullptr, join[8] = {};
     std::vector<cudaEvent_t> ring;          // GFQ_TIMING_RING x 3 events
     int ring_next = 0, ring_count = 0;
     cudaStream_t last_stream = nullptr;
@@ -591,6 +595,9 @@ int gfq_destroy(gfq_handle* h) {
     for (auto& b : h->out) b.release();
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
     for (auto& e : h->ring) if (e) cudaEventDestroy(e);
+    for (auto& e : h->join) if (e) cudaEventDestroy(e);
+    if (h->fork) cudaEventDestroy(h->fork);
+    for (auto& q : h->side) if (q) cudaStreamDestroy(q);
     delete h;
     return GFQ_OK;
 }
@@ -1193,6 +1200,21 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(re[0], st));
     if (h->n_sims > 0) {
         size_t smem = (size_t)h->wpb * h->L.bytes;
+        int active = 0;
+        for (int k = 0; k < NCLASS; k++) active += h->ccount[k] > 0;
+        // several classes: fork onto side streams (not with flows in global
+        // scratch, whose slices are sized for one class at a time)
+        const bool fork = active > 1 && !h->L.flows_global;
+        if (fork) {
+            if (!h->fork) {
+                CK(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
+                for (int k = 0; k < NCLASS; k++) {
+                    CK(cudaStreamCreateWithFlags(&h->side[k], cudaStreamNonBlocking));
+                    CK(cudaEventCreateWithFlags(&h->join[k], cudaEventDisableTiming));
+                }
+            }
+            CK(cudaEventRecord(h->fork, st));
+        }
         int off = 0;
         for (int k = 0; k < NCLASS; k++) {
             if (!h->ccount[k]) continue;
@@ -1202,7 +1224,16 @@ int gfq_launch(gfq_handle* h, void* stream) {
             pk.work = p.work + k;
             dim3 g(h->cblocks[k]), b(k == CLASS_CTA ? h->cta_threads : h->wpb * 32);
             void* args[] = {&pk};
-            CK(cudaLaunchKernel(class_kernel(k, h->L.flows_global), g, b, args, smem, st));
+            cudaStream_t ks = st;
+            if (fork) {
+                ks = h->side[k];
+                CK(cudaStreamWaitEvent(ks, h->fork, 0));
+            }
+            CK(cudaLaunchKernel(class_kernel(k, h->L.flows_global), g, b, args, smem, ks));
+            if (fork) {
+                CK(cudaEventRecord(h->join[k], ks));
+                CK(cudaStreamWaitEvent(st, h->join[k], 0));
+            }
             off += h->ccount[k];
         }
         CK(cudaGetLastError());
