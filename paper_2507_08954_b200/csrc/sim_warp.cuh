@@ -89,9 +89,12 @@ FI u64 wmin64(u64 v) {
 }
 // Store a warp-uniform value to shared memory: every lane has finished
 // reading the old value before any lane writes (RMW-safe under independent
-// thread scheduling), and the write is visible to all lanes afterwards.
+// thread scheduling).  No barrier after the store: every lane writes the same
+// value, so any lane's later load sees that value whichever lane's store it
+// observes (its own is ordered before it).  Blocks of uniform stores below
+// follow the same rule: a __syncwarp() before, none after.
 template <class T>
-FI void ust(T& ref, T v) { __syncwarp(); ref = v; __syncwarp(); }
+FI void ust(T& ref, T v) { __syncwarp(); ref = v; }
 
 // Python max(a, b) / min(a, b): the first argument wins ties.
 FI double pymax(double a, double b) { return b > a ? b : a; }
@@ -484,7 +487,7 @@ struct WarpSim {
         if (GFQ_DIAG && lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
         __syncwarp();
         ev_t()[slot] = t; ev_seq()[slot] = s; ev_meta()[slot] = ((uint32_t)kind << 30) | payload;
-        __syncwarp();
+        // (no trailing sync: every lane stored the same value)
         if (pmin_ok && (pmin_slot < 0 || t < pmin_t || (t == pmin_t && s < pmin_seq))) {
             pmin_t = t; pmin_seq = s; pmin_slot = slot;
         }
@@ -520,7 +523,6 @@ struct WarpSim {
             __syncwarp();
             ev_t()[slot] = t; ev_seq()[slot] = s; ev_meta()[slot] = m;
         }
-        __syncwarp();
         pmin_ok = false;
     }
 
@@ -718,7 +720,6 @@ struct WarpSim {
         RI(d, nr, 0) = inv; RI(d, nr, 1) = fn; RI(d, nr, 2) = st;
         RD(d, nr, 0) = duration; RD(d, nr, 1) = pure;
         DV(d, DV_NRUN) = nr + 1;
-        __syncwarp();
         ust(CNT(d, 2, fn), (uint16_t)(CNT(d, 2, fn) + 1));
         if (!SCRIPTED) ust(DV(d, DV_INSTDIRTY), 1);
     }
@@ -848,7 +849,6 @@ struct WarpSim {
                 if (++sl == WDICT) sl = 0;
             }
             DD(d, DD_INST) = util; DV(d, DV_INSTDIRTY) = 0; DV(d, DV_INSTID) = id;
-            __syncwarp();
         }
         inst = util;
         const int S = P.L.S;
@@ -859,7 +859,6 @@ struct WarpSim {
         int zage = id ? min(DV(d, DV_ZAGE) + 1, 255) : 0;
         __syncwarp();
         SMPT(d, w) = now; SMPU(d, w) = util;
-        __syncwarp();
         double oldt = ns == 0 ? now : DD(d, DD_OLDT);    // time of the oldest sample
         ns++;
         double horizon = now - DD(d, DD_WINDOW);
@@ -902,13 +901,12 @@ struct WarpSim {
             else if (avg < thr - inv) effd = min(effd + 1, dmax);
             hrok = !(avg + inv > thr);                                  // device.py:137-139
         }
-        __syncwarp();
+        if (!ND1) __syncwarp();                          // 1-device build: registers
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
         DV(d, DV_HROK) = hrok; DV(d, DV_ZAGE) = zage;
         DD(d, DD_WCODE) = __longlong_as_double((long long)code);
         DD(d, DD_OLDT) = oldt;
         DD(d, DD_LKEY) = __longlong_as_double((long long)(memo ? key : ~0ull));
-        __syncwarp();
         return effd;
     }
 
@@ -1098,7 +1096,6 @@ struct WarpSim {
             __syncwarp();
             ph()[fn] = k; head()[fn] = nxt; pend()[fn] = pe; infl()[fn] = ninf;
             if (MQFQ) { vt()[fn] = nvt; lex()[fn] = now; }
-            __syncwarp();
             if (BATCH) draining = fn;
             if (MQFQ) {
                 if (gmin_ok && nvt != vt_before && okey(vt_before) == gmin) gmin_ok = false;
@@ -1147,7 +1144,6 @@ struct WarpSim {
         fst()[fn] = s; pt()[fn] = p0 + 1; pend()[fn] = pe + 1;
         vt()[fn] = v; lex()[fn] = le; iat()[fn] = im; head()[fn] = hd;
         if (MQFQ) larr()[fn] = now;
-        __syncwarp();
     }
 
     // on_completion of every policy (mqfq.py:241-247; policies.py:141-142,210-213,264-267)
@@ -1161,7 +1157,6 @@ struct WarpSim {
         __syncwarp();
         done()[fn] = dn; infl()[fn] = inf; tau()[fn] = tm;
         if (MQFQ) lex()[fn] = now;
-        __syncwarp();
         if (MQFQ && pt()[fn] == dn) {                     // queue drained (idle)
             if (gmin_ok && okey(vt()[fn]) == gmin) gmin_ok = false;          // (A)
             idle_lb = pymin(idle_lb, expiry_lb(now, ttl(fn)));               // (B)
