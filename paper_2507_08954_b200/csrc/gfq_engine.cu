@@ -287,7 +287,7 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
     // tick (only when the trace is non-empty) seq n
-    if (w.n > 0 && !scripted) w.push(w.period, EV_TICK, 0);
+    if (w.n > 0 && !scripted) w.push_tick(w.period);
 
     w.run();
     if (CTA) w.cta_release();

@@ -478,10 +478,12 @@ struct WarpSim {
     // ==================================================================
     // event pool (engine.py:83-87: heap of (time, seq, kind, payload))
 
+    // the next monitor tick (now + period, never in the past: period > 0)
+    FI void push_tick(double t) { tick_on = true; tick_t = t; tick_seq = seq++; }
+
     FI void push(double t, int kind, uint32_t payload) {
         if (UNLIKELY(t < now)) { fail(GFQ_SIM_PAST_EVENT); return; }     // engine.py:84-85
         uint32_t s = seq++;
-        if (kind == EV_TICK) { tick_on = true; tick_t = t; tick_seq = s; return; }
         if (UNLIKELY(nev >= P.L.E)) { fail(GFQ_SIM_EVENT_OVERFLOW); return; }
         int slot = nev++;
         if (GFQ_DIAG && lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
@@ -853,7 +855,10 @@ struct WarpSim {
         inst = util;
         const int S = P.L.S;
         int head = DV(d, DV_SHEAD), ns = DV(d, DV_SN);
-        if (UNLIKELY(ns >= S)) { fail(GFQ_SIM_SAMPLE_OVERFLOW); return DV(d, DV_EFFD); }
+        // S = ceil(window / period) + 3 > the samples a window can hold; the
+        // check only guards against a mis-sized ring (the run is failed and
+        // its outputs discarded, so clamping keeps the hot path branch-free)
+        if (UNLIKELY(ns >= S)) { fail(GFQ_SIM_SAMPLE_OVERFLOW); ns = S - 1; }
         int w = head + ns; if (w >= S) w -= S;
         u64 code = ((u64)__double_as_longlong(DD(d, DD_WCODE)) << 4) | (u64)id;
         int zage = id ? min(DV(d, DV_ZAGE) + 1, 255) : 0;
@@ -1293,7 +1298,7 @@ struct WarpSim {
             }
         }
         policy_on_arrival(inv, fn);
-        if (!SCRIPTED && !tick_on) push(now + period, EV_TICK, 0);
+        if (!SCRIPTED && !tick_on) push_tick(now + period);
     }
 
     // Completion stream (InvocationRecords in completion order, read by the
@@ -1357,7 +1362,7 @@ struct WarpSim {
             }
             ps_add(util_sum, inst);
         }
-        if (cursor < n || tot_pend > 0 || tot_infl > 0) push(now + period, EV_TICK, 0);
+        if (cursor < n || tot_pend > 0 || tot_infl > 0) push_tick(now + period);
         else tick_on = false;
     }
 
