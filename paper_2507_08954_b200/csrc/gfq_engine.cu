@@ -246,9 +246,9 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
                 dvd[DD_INVDMAX] = 1.0 / (double)c.d_max;
                 dvi[DV_HROK] = !(0.0 + dvd[DD_INVDMAX] > c.util_threshold);
                 dvi[DV_INSTDIRTY] = 1;                // intern the idle utilization 0.0
-                dvd[DD_LKEY] = __longlong_as_double(-1ll);      // ~0: no previous window
-                u64* wk = (u64*)(base + p.L.o_wkey) + d * WMEMO;
-                for (int k = 0; k < WMEMO; k++) wk[k] = ~0ull;   // no valid key has all bits set
+                dvi[DV_LKEY] = -1;                              // no previous window
+                uint32_t* wk = (uint32_t*)(base + p.L.o_wkey) + d * WMEMO;
+                for (int k = 0; k < WMEMO; k++) wk[k] = 0xffffffffu;   // no valid key has all bits set
                 u64* wd = (u64*)(base + p.L.o_wdict) + d * WDICT;
                 for (int k = 0; k < WDICT; k++) wd[k] = ~0ull;   // empty intern slots
             }

@@ -18,17 +18,18 @@ enum : uint8_t { FL_CREATED = 1, FL_INACTIVE = 2, FL_NEWLY = 4, FL_MARKED = 8 };
 
 // per-device int fields
 enum { DV_OUT = 0, DV_EFFD, DV_HROK, DV_NP, DV_NRUN, DV_SHEAD, DV_SN, DV_INSTDIRTY, DV_INSTID,
-       DV_ZAGE, DV_NSTATE,                                   // hot mutable state (registers
+       DV_ZAGE, DV_WCODE, DV_LKEY, DV_NSTATE,                // hot mutable state (registers
        DV_SPARE0 = DV_NSTATE,                                //  in the 1-device build);
        DV_DMAX, DV_POOLMAX, DV_POOLON, DV_DYN,               //  DeviceConfig copy
-       DV_NI = 16 };
+       DV_NI = 18 };
 // per-device double fields: state, then a copy of the device's DeviceConfig
-enum { DD_UAVG = 0, DD_INST, DD_WCODE, DD_OLDT, DD_LKEY, DD_NSTATE,
+enum { DD_UAVG = 0, DD_INST, DD_OLDT, DD_NSTATE,
        DD_MEMCAP = DD_NSTATE, DD_THR, DD_PCIE, DD_BETA, DD_WINDOW, DD_OVERLAP, DD_INVDMAX,
        DD_ND = 12 };
 // window-average memo: WDICT distinct utilization values per device,
-// WMEMO direct-mapped (window code, count) -> average entries
-enum { WDICT = 15, WMEMO = 16 };
+// WMEMO direct-mapped (window code, count) -> average entries; windows of up
+// to WMAXN samples are memoised (32-bit key: 7 x 4-bit ids + the count)
+enum { WDICT = 15, WMEMO = 16, WMAXN = 7 };
 // flows queued for swap-out since the last _swap_out_inactive
 enum { NEWLY_CAP = 32 };
 // per-warp diagnostic counters (shared memory, lane 0 increments)
@@ -70,7 +71,7 @@ struct Layout {
     int32_t o_smp_t, o_smp_u;                            // f64[ND][S]
     int32_t o_run_i, o_run_d;                            // i32[ND][R][4], f64[ND][R][2]
     int32_t o_pool_m, o_pool_t;                          // u32[ND][P], f64[ND][P]
-    int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u64[ND][WMEMO], f64[ND][WMEMO]
+    int32_t o_wdict, o_wkey, o_wval;                     // f64[ND][WDICT], u32[ND][WMEMO], f64[ND][WMEMO]
     int32_t o_diag;                                      // u32[DG_N]
     int32_t o_newly;                                     // i32[NEWLY_CAP]
     int32_t o_cst, o_csp, o_csm;                         // completion staging: f64[32], i32[32], i32[32]
@@ -157,7 +158,7 @@ inline void layout_finish(Layout& L) {
     L.o_smp_t = take(8 * ND * S); L.o_smp_u = take(8 * ND * S);
     L.o_run_i = take(4 * 4 * ND * R); L.o_run_d = take(8 * 2 * ND * R);
     L.o_pool_m = take(4 * ND * P); L.o_pool_t = take(8 * ND * P);
-    L.o_wdict = take(8 * WDICT * ND); L.o_wkey = take(8 * WMEMO * ND); L.o_wval = take(8 * WMEMO * ND);
+    L.o_wdict = take(8 * WDICT * ND); L.o_wkey = take(4 * WMEMO * ND); L.o_wval = take(8 * WMEMO * ND);
     L.o_diag = take(4 * DG_N);
     L.o_newly = take(4 * NEWLY_CAP);
     L.o_cta = L.cta ? take((int32_t)sizeof(CtaCmd)) : 0;

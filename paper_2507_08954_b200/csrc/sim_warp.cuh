@@ -226,7 +226,7 @@ struct WarpSim {
     FI uint32_t& PM(int d, int i) const { return ((uint32_t*)(sm + P.L.o_pool_m))[d * P.L.P + i]; }
     FI double& PT(int d, int i) const { return ((double*)(sm + P.L.o_pool_t))[d * P.L.P + i]; }
     FI double& WDICTV(int d, int i) const { return ((double*)(sm + P.L.o_wdict))[d * WDICT + i]; }
-    FI u64& WKEY(int d, int i) const { return ((u64*)(sm + P.L.o_wkey))[d * WMEMO + i]; }
+    FI uint32_t& WKEY(int d, int i) const { return ((uint32_t*)(sm + P.L.o_wkey))[d * WMEMO + i]; }
     FI double& WVAL(int d, int i) const { return ((double*)(sm + P.L.o_wval))[d * WMEMO + i]; }
     FI int* NEWLY() const { return (int*)(sm + P.L.o_newly); }
     FI double* CST() const { return (double*)(sm + P.L.o_cst); }      // completion staging
@@ -860,8 +860,8 @@ struct WarpSim {
         // its outputs discarded, so clamping keeps the hot path branch-free)
         if (UNLIKELY(ns >= S)) { fail(GFQ_SIM_SAMPLE_OVERFLOW); ns = S - 1; }
         int w = head + ns; if (w >= S) w -= S;
-        u64 code = ((u64)__double_as_longlong(DD(d, DD_WCODE)) << 4) | (u64)id;
-        int zage = id ? min(DV(d, DV_ZAGE) + 1, 255) : 0;
+        const uint32_t code = ((uint32_t)DV(d, DV_WCODE) << 4) | (uint32_t)id;
+        const int zage = id ? min(DV(d, DV_ZAGE) + 1, 15) : 0;
         __syncwarp();
         SMPT(d, w) = now; SMPU(d, w) = util;
         double oldt = ns == 0 ? now : DD(d, DD_OLDT);    // time of the oldest sample
@@ -873,14 +873,15 @@ struct WarpSim {
             oldt = SMPT(d, head);                          // ns >= 1: the new sample stays
         }
         double avg;
-        bool memo = ns <= 14 && zage >= ns;          // key ~0 stays the empty-slot marker
-        u64 key = 0; int slot = 0;
+        // memo key: the window's ids and count (valid while the last ns ids
+        // are all interned); 0xffffffff (never a key: count <= 7) marks empty
+        const bool memo = ns <= WMAXN && zage >= ns;
+        uint32_t key = 0xffffffffu; int slot = 0;
         if (memo) {
-            key = (code & ((1ull << (4 * ns)) - 1)) | ((u64)ns << 60);
-            slot = (int)((((uint32_t)key ^ (uint32_t)(key >> 32)) * 0x9E3779B1u) >> 28);
+            key = (code & ((1u << (4 * ns)) - 1u)) | ((uint32_t)ns << 28);
+            slot = (int)((key * 0x9E3779B1u) >> 28);
         }
-        const u64 lkey = (u64)__double_as_longlong(DD(d, DD_LKEY));
-        if (memo && key == lkey) {                    // same window as the last tick
+        if (memo && key == (uint32_t)DV(d, DV_LKEY)) {  // same window as the last tick
             avg = UAVG(d);
         } else if (LIKELY(memo && WKEY(d, slot) == key)) {
             avg = WVAL(d, slot);
@@ -892,7 +893,7 @@ struct WarpSim {
             #pragma unroll 1
             for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
             avg = ps_val(a) / (double)ns;
-            if (memo) { __syncwarp(); WKEY(d, slot) = key; WVAL(d, slot) = avg; __syncwarp(); }
+            if (memo) { __syncwarp(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
         }
         int effd = DV(d, DV_EFFD), hrok = DV(d, DV_HROK);
         const bool dyn = DV(d, DV_DYN);
@@ -909,9 +910,8 @@ struct WarpSim {
         if (!ND1) __syncwarp();                          // 1-device build: registers
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
         DV(d, DV_HROK) = hrok; DV(d, DV_ZAGE) = zage;
-        DD(d, DD_WCODE) = __longlong_as_double((long long)code);
+        DV(d, DV_WCODE) = (int)code; DV(d, DV_LKEY) = (int)key;
         DD(d, DD_OLDT) = oldt;
-        DD(d, DD_LKEY) = __longlong_as_double((long long)(memo ? key : ~0ull));
         return effd;
     }
 
@@ -1360,7 +1360,9 @@ struct WarpSim {
                 P.util_rows[o * 3 + 2] = UAVG(d);
                 P.util_meta[o * 2 + 0] = d; P.util_meta[o * 2 + 1] = eff;
             }
-            ps_add(util_sum, inst);
+            // adding +0.0 (nothing running) leaves a Neumaier sum of
+            // non-negative terms bit-for-bit unchanged
+            if (inst != 0.0) ps_add(util_sum, inst);
         }
         if (cursor < n || tot_pend > 0 || tot_infl > 0) push_tick(now + period);
         else tick_on = false;
