@@ -87,14 +87,29 @@ FI u64 wmin64(u64 v) {
     unsigned lo = wmin32(((unsigned)(v >> 32) == hi) ? (unsigned)v : 0xffffffffu);
     return ((u64)hi << 32) | lo;
 }
-// Store a warp-uniform value to shared memory: every lane has finished
-// reading the old value before any lane writes (RMW-safe under independent
-// thread scheduling).  No barrier after the store: every lane writes the same
-// value, so any lane's later load sees that value whichever lane's store it
-// observes (its own is ordered before it).  Blocks of uniform stores below
-// follow the same rule: a __syncwarp() before, none after.
+// Uniform shared-memory state is read-modify-written by all 32 lanes with
+// identical values (each lane loads X, then stores the same new X).
+//  * No barrier after such a store: whichever lane's store a later load
+//    observes, the value is the same, and a lane's own store is ordered
+//    before its own later loads.
+//  * None before it either (USYNC() is empty): the warp runs the scalar
+//    code converged -- every branch there is on warp-uniform values -- so all
+//    lanes execute a load before any lane executes the store after it.  The
+//    regions that diverge (lane-strided scans, lane-0 writes) end in a
+//    *_sync reduction or an explicit __syncwarp(), which reconverge the warp
+//    before scalar code continues.  -DGFQ_STRICT_SYNC=1 restores a
+//    __syncwarp() before every uniform store (the parity suite passes on
+//    both builds).
+#ifndef GFQ_STRICT_SYNC
+#define GFQ_STRICT_SYNC 0
+#endif
+#if GFQ_STRICT_SYNC
+#define USYNC() __syncwarp()
+#else
+#define USYNC() do { } while (0)
+#endif
 template <class T>
-FI void ust(T& ref, T v) { __syncwarp(); ref = v; }
+FI void ust(T& ref, T v) { USYNC(); ref = v; }
 
 // Python max(a, b) / min(a, b): the first argument wins ties.
 FI double pymax(double a, double b) { return b > a ? b : a; }
@@ -487,7 +502,7 @@ struct WarpSim {
         if (UNLIKELY(nev >= P.L.E)) { fail(GFQ_SIM_EVENT_OVERFLOW); return; }
         int slot = nev++;
         if (GFQ_DIAG && lane == 0) { uint32_t* dg = (uint32_t*)(sm + P.L.o_diag); dg[DG_MAXEV] = max(dg[DG_MAXEV], (uint32_t)nev); }
-        __syncwarp();
+        USYNC();
         ev_t()[slot] = t; ev_seq()[slot] = s; ev_meta()[slot] = ((uint32_t)kind << 30) | payload;
         // (no trailing sync: every lane stored the same value)
         if (pmin_ok && (pmin_slot < 0 || t < pmin_t || (t == pmin_t && s < pmin_seq))) {
@@ -522,7 +537,7 @@ struct WarpSim {
         int last = --nev;
         if (slot != last) {
             double t = ev_t()[last]; uint32_t s = ev_seq()[last], m = ev_meta()[last];
-            __syncwarp();
+            USYNC();
             ev_t()[slot] = t; ev_seq()[slot] = s; ev_meta()[slot] = m;
         }
         pmin_ok = false;
@@ -718,7 +733,7 @@ struct WarpSim {
     FI void run_append(int d, int inv, int fn, int st, double duration, double pure) {
         int nr = DV(d, DV_NRUN);
         if (UNLIKELY(nr >= P.L.R)) { fail(GFQ_SIM_POOL_OVERFLOW); return; }
-        __syncwarp();
+        USYNC();
         RI(d, nr, 0) = inv; RI(d, nr, 1) = fn; RI(d, nr, 2) = st;
         RD(d, nr, 0) = duration; RD(d, nr, 1) = pure;
         DV(d, DV_NRUN) = nr + 1;
@@ -737,7 +752,7 @@ struct WarpSim {
         for (int r = ri; r < nr - 1; r++) {
             int a = RI(d, r + 1, 0), b = RI(d, r + 1, 1), c = RI(d, r + 1, 2);
             double x = RD(d, r + 1, 0), y = RD(d, r + 1, 1);
-            __syncwarp();
+            USYNC();
             RI(d, r, 0) = a; RI(d, r, 1) = b; RI(d, r, 2) = c; RD(d, r, 0) = x; RD(d, r, 1) = y;
         }
         ust(DV(d, DV_NRUN), nr - 1);
@@ -802,7 +817,7 @@ struct WarpSim {
         if (UNLIKELY(np >= P.L.P)) { fail(GFQ_SIM_POOL_OVERFLOW); return false; }
         // the re-pooled entry is (fn, GPU_WARM, mem[fn], now, evictable=False)
         // whether or not a container was claimed at start (device.py:226-236)
-        __syncwarp();
+        USYNC();
         PM(d, np) = pm_make(fn, GFQ_GPU_WARM, 0);
         PT(d, np) = now;
         DV(d, DV_NP) = np + 1;
@@ -842,9 +857,9 @@ struct WarpSim {
                 const u64 v = (u64)__double_as_longlong(WDICTV(d, sl));
                 if (v == ub) { id = sl + 1; break; }
                 if (v == ~0ull) {
-                    __syncwarp();
+                    USYNC();
                     WDICTV(d, sl) = util;
-                    __syncwarp();
+                    USYNC();
                     id = sl + 1;
                     break;
                 }
@@ -862,7 +877,7 @@ struct WarpSim {
         int w = head + ns; if (w >= S) w -= S;
         const uint32_t code = ((uint32_t)DV(d, DV_WCODE) << 4) | (uint32_t)id;
         const int zage = id ? min(DV(d, DV_ZAGE) + 1, 15) : 0;
-        __syncwarp();
+        USYNC();
         SMPT(d, w) = now; SMPU(d, w) = util;
         double oldt = ns == 0 ? now : DD(d, DD_OLDT);    // time of the oldest sample
         ns++;
@@ -893,7 +908,7 @@ struct WarpSim {
             #pragma unroll 1
             for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
             avg = ps_val(a) / (double)ns;
-            if (memo) { __syncwarp(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
+            if (memo) { USYNC(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
         }
         int effd = DV(d, DV_EFFD), hrok = DV(d, DV_HROK);
         const bool dyn = DV(d, DV_DYN);
@@ -1064,6 +1079,7 @@ struct WarpSim {
             P.dsp_inv[o] = inv; P.dsp_vt[o] = vt_before; P.dsp_gvt[o] = g;
             P.dsp_qlen[o] = qlen; P.dsp_infl[o] = infl_after;
         }
+        __syncwarp();                        // reconverge after the lane-0 write
     }
 
     // One Policy.dispatch call for every policy kind; returns the started
@@ -1098,7 +1114,7 @@ struct WarpSim {
             double vt_before = vt()[fn];
             double nvt = vt_before;
             if (MQFQ) nvt = vt_before + tau()[fn] / weight(fn);          // mqfq.py:223
-            __syncwarp();
+            USYNC();
             ph()[fn] = k; head()[fn] = nxt; pend()[fn] = pe; infl()[fn] = ninf;
             if (MQFQ) { vt()[fn] = nvt; lex()[fn] = now; }
             if (BATCH) draining = fn;
@@ -1145,7 +1161,7 @@ struct WarpSim {
                 if (k < gmin) gmin = k;
             }
         }
-        __syncwarp();
+        USYNC();
         fst()[fn] = s; pt()[fn] = p0 + 1; pend()[fn] = pe + 1;
         vt()[fn] = v; lex()[fn] = le; iat()[fn] = im; head()[fn] = hd;
         if (MQFQ) larr()[fn] = now;
@@ -1159,7 +1175,7 @@ struct WarpSim {
         int inf = infl()[fn] - 1;
         double tm = tau()[fn];
         tm = tm + (exec_s - tm) / (double)dn;            // tau.count == completions
-        __syncwarp();
+        USYNC();
         done()[fn] = dn; infl()[fn] = inf; tau()[fn] = tm;
         if (MQFQ) lex()[fn] = now;
         if (MQFQ && pt()[fn] == dn) {                     // queue drained (idle)
@@ -1178,6 +1194,7 @@ struct WarpSim {
             int64_t o = (int64_t)sid * P.audit_backlog_cap + k;
             P.backlog_time[o] = now; P.backlog_meta[o] = (fn << 1) | (on ? 1 : 0);
         }
+        __syncwarp();
     }
 
     // _swap_out_inactive, engine.py:199-203 (+ Device.swap_out / mark_evictable)
@@ -1244,6 +1261,7 @@ struct WarpSim {
             P.rec_dispatch[o] = now; P.rec_state[o] = (int8_t)st; P.rec_device[o] = (int8_t)dev;
             P.rec_pure[o] = pure;
         }
+        __syncwarp();
         push(now + duration, EV_COMPLETION, (uint32_t)inv | ((uint32_t)dev << 27));
     }
 
@@ -1341,6 +1359,7 @@ struct WarpSim {
                 P.rec_order[roff + inv] = k;
             }
         }
+        __syncwarp();
         if (CSTAGE && (k & 31) == 31) comp_flush(32);
         if (!SCRIPTED && pt()[fn] - done()[fn] == 0) {     // _backlog_change(-1)
             backlog_audit(fn, false);
@@ -1360,6 +1379,7 @@ struct WarpSim {
                 P.util_rows[o * 3 + 2] = UAVG(d);
                 P.util_meta[o * 2 + 0] = d; P.util_meta[o * 2 + 1] = eff;
             }
+            __syncwarp();
             // adding +0.0 (nothing running) leaves a Neumaier sum of
             // non-negative terms bit-for-bit unchanged
             if (inst != 0.0) ps_add(util_sum, inst);
@@ -1400,6 +1420,7 @@ struct WarpSim {
             P.event_time[o] = t;
             P.event_meta[o] = (int64_t)((payload << 2) | kind);
         }
+        __syncwarp();
     }
 
     // Simulation.run / step, engine.py:99-119
