@@ -1467,6 +1467,12 @@ struct WarpSim {
                 // (one counted dispatch() call, no state change) and the next
                 // event is again the tick, stay in this loop.  A tick whose drain
                 // may dispatch falls through to the common drain() below.
+                // During the run nothing but the tick is pushed, so the next
+                // arrival and the pooled minimum stay put, and both win a
+                // time tie with the tick (an arrival's seq is its trace index;
+                // a pooled event was pushed before the tick): the run ends at
+                // the first tick with time >= lim.
+                const double lim = pymin(t_arr, pmin_slot >= 0 ? pmin_t : INF);
                 #pragma unroll 1
                 for (;;) {
                     tick_on = false;
@@ -1477,10 +1483,7 @@ struct WarpSim {
                     n_calls++;
                     diag(DG_QUIET);
                     dr = false;
-                    if (!tick_on || UNLIKELY(n_events >= max_events)) break;
-                    if (t_arr <= tick_t) break;                       // an arrival comes first
-                    if (pmin_slot >= 0 && (pmin_t < tick_t || (pmin_t == tick_t && pmin_seq < tick_seq)))
-                        break;                                        // a pooled event comes first
+                    if (!tick_on || UNLIKELY(n_events >= max_events) || tick_t >= lim) break;
                     now = tick_t;
                     n_events++;
                     dr = true;
