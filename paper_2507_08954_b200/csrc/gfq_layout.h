@@ -29,7 +29,7 @@ enum { DD_UAVG = 0, DD_INST, DD_OLDT, DD_NSTATE,
 // window-average memo: WDICT distinct utilization values per device,
 // WMEMO direct-mapped (window code, count) -> average entries; windows of up
 // to WMAXN samples are memoised (32-bit key: 7 x 4-bit ids + the count)
-enum { WDICT = 15, WMEMO = 16, WMAXN = 7 };
+enum { WDICT = 15, WMEMO = 64, WMEMO_BITS = 6, WMAXN = 7 };
 // flows queued for swap-out since the last _swap_out_inactive
 enum { NEWLY_CAP = 32 };
 // per-warp diagnostic counters (shared memory, lane 0 increments)

@@ -894,7 +894,7 @@ struct WarpSim {
         uint32_t key = 0xffffffffu; int slot = 0;
         if (memo) {
             key = (code & ((1u << (4 * ns)) - 1u)) | ((uint32_t)ns << 28);
-            slot = (int)((key * 0x9E3779B1u) >> 28);
+            slot = (int)((key * 0x9E3779B1u) >> (32 - WMEMO_BITS));
         }
         if (memo && key == (uint32_t)DV(d, DV_LKEY)) {  // same window as the last tick
             avg = UAVG(d);
