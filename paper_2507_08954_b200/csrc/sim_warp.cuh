@@ -841,7 +841,9 @@ struct WarpSim {
     // window order; it is memoised exactly: each device interns its distinct
     // sample values (<= WDICT) as 4-bit ids, the window is the shift register
     // of the ids of its samples, and (ids, count) fixes the summed sequence.
-    FI int monitor_tick(int d, double& inst) {
+    // The tick's utilization sample (instantaneous_util, cached while the
+    // running set is unchanged) and its interned id.
+    FI double tick_util(int d, int& id_out) {
         double util = DD(d, DD_INST);
         int id = DV(d, DV_INSTID);
         if (DV(d, DV_INSTDIRTY)) {              // the running set changed since the last tick
@@ -867,7 +869,11 @@ struct WarpSim {
             }
             DD(d, DD_INST) = util; DV(d, DV_INSTDIRTY) = 0; DV(d, DV_INSTID) = id;
         }
-        inst = util;
+        id_out = id;
+        return util;
+    }
+
+    FI int monitor_tick(int d, double util, int id) {
         const int S = P.L.S;
         int head = DV(d, DV_SHEAD), ns = DV(d, DV_SN);
         // S = ceil(window / period) + 3 > the samples a window can hold; the
@@ -1074,12 +1080,14 @@ struct WarpSim {
 
     FI void audit_dispatch(int inv, double vt_before, double g, int qlen, int infl_after) {
         int k = n_disp++;
-        if ((P.outputs & GFQ_WANT_DISPATCH) && lane == 0) {
-            int64_t o = roff + k;
-            P.dsp_inv[o] = inv; P.dsp_vt[o] = vt_before; P.dsp_gvt[o] = g;
-            P.dsp_qlen[o] = qlen; P.dsp_infl[o] = infl_after;
+        if (P.outputs & GFQ_WANT_DISPATCH) {
+            if (lane == 0) {
+                int64_t o = roff + k;
+                P.dsp_inv[o] = inv; P.dsp_vt[o] = vt_before; P.dsp_gvt[o] = g;
+                P.dsp_qlen[o] = qlen; P.dsp_infl[o] = infl_after;
+            }
+            __syncwarp();                    // reconverge after the lane-0 write
         }
-        __syncwarp();                        // reconverge after the lane-0 write
     }
 
     // One Policy.dispatch call for every policy kind; returns the started
@@ -1194,7 +1202,7 @@ struct WarpSim {
             int64_t o = (int64_t)sid * P.audit_backlog_cap + k;
             P.backlog_time[o] = now; P.backlog_meta[o] = (fn << 1) | (on ? 1 : 0);
         }
-        __syncwarp();
+        if (G) __syncwarp();
     }
 
     // _swap_out_inactive, engine.py:199-203 (+ Device.swap_out / mark_evictable)
@@ -1256,12 +1264,14 @@ struct WarpSim {
             start_invocation(dev, fn, st, inv, duration, pure);
         }
         if (status) return;
-        if ((P.outputs & GFQ_WANT_RECORDS) && lane == 0) {
-            int64_t o = roff + inv;
-            P.rec_dispatch[o] = now; P.rec_state[o] = (int8_t)st; P.rec_device[o] = (int8_t)dev;
-            P.rec_pure[o] = pure;
+        if (P.outputs & GFQ_WANT_RECORDS) {
+            if (lane == 0) {
+                int64_t o = roff + inv;
+                P.rec_dispatch[o] = now; P.rec_state[o] = (int8_t)st; P.rec_device[o] = (int8_t)dev;
+                P.rec_pure[o] = pure;
+            }
+            __syncwarp();
         }
-        __syncwarp();
         push(now + duration, EV_COMPLETION, (uint32_t)inv | ((uint32_t)dev << 27));
     }
 
@@ -1370,8 +1380,13 @@ struct WarpSim {
     FI void on_monitor() {                                // engine.py:155-165
         #pragma unroll 1
         for (int d = 0; d < NDEV(); d++) {
-            double inst;
-            int eff = monitor_tick(d, inst);
+            int id;
+            const double inst = tick_util(d, id);
+            // the mean-utilization sum first: its fp64 chain overlaps the
+            // window work below (adding +0.0, nothing running, leaves a
+            // Neumaier sum of non-negative terms bit-for-bit unchanged)
+            if (inst != 0.0) ps_add(util_sum, inst);
+            int eff = monitor_tick(d, inst, id);
             int k = n_util++;
             if ((G && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_util_cap) {
                 int64_t o = (int64_t)sid * P.audit_util_cap + k;
@@ -1379,10 +1394,7 @@ struct WarpSim {
                 P.util_rows[o * 3 + 2] = UAVG(d);
                 P.util_meta[o * 2 + 0] = d; P.util_meta[o * 2 + 1] = eff;
             }
-            __syncwarp();
-            // adding +0.0 (nothing running) leaves a Neumaier sum of
-            // non-negative terms bit-for-bit unchanged
-            if (inst != 0.0) ps_add(util_sum, inst);
+            if (G) __syncwarp();
         }
         if (cursor < n || tot_pend > 0 || tot_infl > 0) push_tick(now + period);
         else tick_on = false;
@@ -1420,7 +1432,7 @@ struct WarpSim {
             P.event_time[o] = t;
             P.event_meta[o] = (int64_t)((payload << 2) | kind);
         }
-        __syncwarp();
+        if (G) __syncwarp();
     }
 
     // Simulation.run / step, engine.py:99-119
