@@ -253,20 +253,27 @@ def run_gfq(args):
     info = eng.batch_info()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
-    hist_t = None
+    hist_t = summ_t = None
     if world > 1:
         ptr, n = eng.output_device_ptr(_abi.OUT_HIST)
         hist_t = torch.as_tensor(_CudaArray(ptr, n, "<i8"), device="cuda")
+        ptr, n = eng.output_device_ptr(_abi.OUT_SUMMARY)
+        summ_t = torch.as_tensor(_CudaArray(ptr, n, "<f8"), device="cuda").view(-1, 3)
+    from paper_2507_08954_b200.dist import gather_rows
 
     def step():
         eng.launch(stream)
         if hist_t is not None:
+            # the one collective step: latency histograms summed,
+            # per-simulation summary rows gathered, over NVLink (NCCL)
             if backend == "nccl":
-                dist.all_reduce(hist_t)   # histogram gather over NVLink (NCCL)
+                dist.all_reduce(hist_t)
+                gather_rows(summ_t)
             else:
                 h = hist_t.cpu()
                 dist.all_reduce(h)
                 hist_t.copy_(h)
+                gather_rows(summ_t.cpu())
 
     for _ in range(max(args.warmup, 0)):
         flush.fill_(1)
