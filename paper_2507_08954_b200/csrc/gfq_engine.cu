@@ -737,6 +737,7 @@ int gfq_generate_traces(gfq_handle* h, int32_t n_traces, const int32_t* n_functi
         toff[t + 1] = total;
         if (toff[t + 1] - toff[t] >= (1 << 27)) return set_err(GFQ_EINVAL, "gfq_generate_traces: trace longer than 2^27 arrivals");
     }
+    if (total >= ((int64_t)1 << 31)) return set_err(GFQ_EINVAL, "gfq_generate_traces: more than 2^31 arrivals in one call");
     const size_t na = (size_t)std::max<int64_t>(total, 1);
     if ((rc = d_k0.ensure(8 * na)) || (rc = d_k1.ensure(8 * na)) || (rc = d_v0.ensure(4 * na)) || (rc = d_v1.ensure(4 * na)))
         return rc;
@@ -1026,7 +1027,6 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
             const double need = (double)per_sm * (double)(smem + 1024);
             int pct = (int)ceil(100.0 * need / (double)h->smem_per_sm);
             pct = std::min(100, std::max(pct, 1));
-            if (getenv("GFQ_CARVEOUT")) pct = atoi(getenv("GFQ_CARVEOUT"));
             CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
             int per_sm2 = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kfn, threads, smem));
