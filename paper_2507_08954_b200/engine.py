@@ -287,6 +287,19 @@ class Engine:
                                           n.value * b.value))
         return a
 
+    def output_into(self, oid: int, out: np.ndarray) -> np.ndarray:
+        """Copy output `oid` into a caller-owned array (e.g. pinned host
+        memory, for full-bandwidth device->host reads); returns the filled
+        prefix view."""
+        n, b = C.c_int64(), C.c_int32()
+        check(self._L.gfq_output_info(self._h, oid, C.byref(n), C.byref(b)))
+        if out.dtype != _OUT_DTYPES[oid] or out.size < n.value or not out.flags.c_contiguous:
+            raise ValueError("output_into: array too small, wrong dtype or not contiguous")
+        if n.value:
+            check(self._L.gfq_output_copy(self._h, oid, out.ctypes.data_as(C.c_void_p),
+                                          n.value * b.value))
+        return out[: n.value]
+
     def output_device_ptr(self, oid: int) -> tuple[int, int]:
         p = C.c_void_p()
         n, b = C.c_int64(), C.c_int32()
