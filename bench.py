@@ -253,8 +253,17 @@ def run_gfq(args):
     info = eng.batch_info()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
-    hist_t = summ_t = None
-    if world > 1:
+    hist_t = summ_t = comm = summ_all = None
+    if world > 1 and backend == "nccl":
+        # the one collective step through the C ABI
+        # (gfq_reduce_nccl): histograms all-reduced, summary rows all-gathered
+        # over NVLink; the communicator's id travels over torch.distributed
+        from paper_2507_08954_b200.engine import NcclComm
+        uid = [NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = NcclComm(world, rank, uid[0])
+        summ_all = torch.empty(world * len(w.sims) * 3, dtype=torch.float64, device="cuda")
+    elif world > 1:
         ptr, n = eng.output_device_ptr(_abi.OUT_HIST)
         hist_t = torch.as_tensor(_CudaArray(ptr, n, "<i8"), device="cuda")
         ptr, n = eng.output_device_ptr(_abi.OUT_SUMMARY)
@@ -263,17 +272,13 @@ def run_gfq(args):
 
     def step():
         eng.launch(stream)
-        if hist_t is not None:
-            # the one collective step: latency histograms summed,
-            # per-simulation summary rows gathered, over NVLink (NCCL)
-            if backend == "nccl":
-                dist.all_reduce(hist_t)
-                gather_rows(summ_t)
-            else:
-                h = hist_t.cpu()
-                dist.all_reduce(h)
-                hist_t.copy_(h)
-                gather_rows(summ_t.cpu())
+        if comm is not None:
+            eng.reduce_nccl(comm, summ_all, stream)
+        elif hist_t is not None:          # gloo (the multi-rank path on one GPU)
+            h = hist_t.cpu()
+            dist.all_reduce(h)
+            hist_t.copy_(h)
+            gather_rows(summ_t.cpu())
 
     for _ in range(max(args.warmup, 0)):
         flush.fill_(1)
@@ -328,6 +333,9 @@ def run_gfq(args):
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     e2e = e2e_run(eng, w, outputs, kw, e2e_steps, world, dist if world > 1 else None)
 
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -303,6 +303,22 @@ int  gfq_output_device_ptr(gfq_handle* h, int32_t id, void** dptr);
 int  gfq_fairness(gfq_handle* h, double window_s, const int32_t* d_max,
                   const double* report_weight, int64_t n_weights);
 
+/* ---- multi-GPU (one process per GPU) -------------------------------------
+ * The sweep's one collective step: after a launch, sum the
+ * latency histograms of every rank in place (ncclAllReduce) and gather every
+ * rank's per-simulation summary rows (ncclAllGather) into summary_out, a
+ * device buffer of n_ranks * n_sims * 3 doubles (NULL: histograms only).
+ * Enqueued on `stream` (cudaStream_t, NULL = legacy default) after the
+ * launch; all ranks must have staged batches of the same shape.  NCCL is
+ * loaded at first use (dlopen "libnccl.so.2", the one already in the process
+ * if any); comm is an ncclComm_t, from the helpers below or the caller's own.
+ * Replaces the serial per-process result collection of cli.cmd_sweep. */
+#define GFQ_NCCL_ID_BYTES 128
+int  gfq_nccl_unique_id(char id[GFQ_NCCL_ID_BYTES]);
+int  gfq_nccl_comm_init(void** comm, int32_t n_ranks, const char id[GFQ_NCCL_ID_BYTES], int32_t rank);
+int  gfq_nccl_comm_destroy(void* comm);
+int  gfq_reduce_nccl(gfq_handle* h, void* comm, void* summary_out, void* stream);
+
 /* Convenience: prepare + launch + synchronize on the default stream.
  * The drop-in for run_simulation over a batch (engine.py:214-218). */
 int  gfq_run(gfq_handle* h, const gfq_sim* sims, int32_t n_sims,

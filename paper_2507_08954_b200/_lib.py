@@ -42,6 +42,10 @@ _SIGS = {
                                       _P(C.c_int32), _P(C.c_double), _P(C.c_uint64),
                                       _P(C.c_uint8), _P(C.c_int64)]),
     "gfq_download_traces": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_int32), C.c_int64]),
+    "gfq_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "gfq_nccl_comm_init": (C.c_int, [_P(C.c_void_p), C.c_int32, C.c_char_p, C.c_int32]),
+    "gfq_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "gfq_reduce_nccl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gfq_kernel_times": (C.c_int, [C.c_void_p, _P(C.c_float), _P(C.c_float), C.c_int32,
                                    _P(C.c_int32)]),
     "gfq_output_info": (C.c_int, [C.c_void_p, C.c_int32, _P(C.c_int64), _P(C.c_int32)]),

@@ -20,7 +20,7 @@ OUT = os.path.join(HERE, "libgfq.so")
 SRC = os.path.join(HERE, "csrc", "gfq_engine.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-         "-shared", f"-I{ROOT}/include"]
+         "-shared", f"-I{ROOT}/include", "-ldl"]
 
 
 def nvcc() -> str:

@@ -22,6 +22,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <string>
@@ -1310,6 +1312,97 @@ int gfq_batch_info(gfq_handle* h, int32_t* info, int32_t n) {
         if (h->ccount[k]) { v[0]++; v[4] = std::max(v[4], h->cblocks[k]); }
     if (h->n_sims > 0) v[0]++;                             // k_reduce
     for (int i = 0; i < n; i++) info[i] = v[i];
+    return GFQ_OK;
+}
+
+// ---- NCCL, loaded at first use (no link-time dependency)
+namespace {
+struct NcclId { char internal[GFQ_NCCL_ID_BYTES]; };    // ncclUniqueId (passed by value)
+struct NcclApi {
+    typedef int (*GetId)(NcclId*);
+    typedef int (*InitRank)(void**, int, NcclId, int);
+    typedef int (*Destroy)(void*);
+    typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+    typedef int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t);
+    typedef int (*Group)();
+    typedef const char* (*ErrStr)(int);
+    GetId get_id = nullptr; InitRank init_rank = nullptr; Destroy destroy = nullptr;
+    AllReduce all_reduce = nullptr; AllGather all_gather = nullptr;
+    Group group_start = nullptr, group_end = nullptr; ErrStr err = nullptr;
+    bool ok = false, tried = false;
+};
+NcclApi g_nccl;
+// nccl.h enums (stable across NCCL 2.x)
+enum { NCCL_UINT64 = 5, NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
+
+int nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok ? GFQ_OK : set_err(GFQ_ERUNTIME, "NCCL is not available (libnccl.so.2)");
+    g_nccl.tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return set_err(GFQ_ERUNTIME, std::string("dlopen libnccl.so.2: ") + dlerror());
+    g_nccl.get_id = (NcclApi::GetId)dlsym(lib, "ncclGetUniqueId");
+    g_nccl.init_rank = (NcclApi::InitRank)dlsym(lib, "ncclCommInitRank");
+    g_nccl.destroy = (NcclApi::Destroy)dlsym(lib, "ncclCommDestroy");
+    g_nccl.all_reduce = (NcclApi::AllReduce)dlsym(lib, "ncclAllReduce");
+    g_nccl.all_gather = (NcclApi::AllGather)dlsym(lib, "ncclAllGather");
+    g_nccl.group_start = (NcclApi::Group)dlsym(lib, "ncclGroupStart");
+    g_nccl.group_end = (NcclApi::Group)dlsym(lib, "ncclGroupEnd");
+    g_nccl.err = (NcclApi::ErrStr)dlsym(lib, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.get_id && g_nccl.init_rank && g_nccl.destroy && g_nccl.all_reduce &&
+                g_nccl.all_gather && g_nccl.group_start && g_nccl.group_end && g_nccl.err;
+    return g_nccl.ok ? GFQ_OK : set_err(GFQ_ERUNTIME, "libnccl.so.2 lacks the expected symbols");
+}
+
+#define NK(call)                                                                            \
+    do {                                                                                    \
+        int r_ = (call);                                                                    \
+        if (r_ != 0) return set_err(GFQ_ERUNTIME, std::string(#call) + ": " + g_nccl.err(r_)); \
+    } while (0)
+}  // namespace
+
+int gfq_nccl_unique_id(char id[GFQ_NCCL_ID_BYTES]) {
+    if (!id) return set_err(GFQ_EINVAL, "gfq_nccl_unique_id: null id");
+    int rc = nccl_load();
+    if (rc) return rc;
+    NcclId u;
+    NK(g_nccl.get_id(&u));
+    memcpy(id, u.internal, GFQ_NCCL_ID_BYTES);
+    return GFQ_OK;
+}
+
+int gfq_nccl_comm_init(void** comm, int32_t n_ranks, const char id[GFQ_NCCL_ID_BYTES], int32_t rank) {
+    if (!comm || !id || n_ranks < 1 || rank < 0 || rank >= n_ranks)
+        return set_err(GFQ_EINVAL, "gfq_nccl_comm_init: bad arguments");
+    int rc = nccl_load();
+    if (rc) return rc;
+    NcclId u;
+    memcpy(u.internal, id, GFQ_NCCL_ID_BYTES);
+    NK(g_nccl.init_rank(comm, n_ranks, u, rank));
+    return GFQ_OK;
+}
+
+int gfq_nccl_comm_destroy(void* comm) {
+    if (!comm) return GFQ_OK;
+    int rc = nccl_load();
+    if (rc) return rc;
+    NK(g_nccl.destroy(comm));
+    return GFQ_OK;
+}
+
+int gfq_reduce_nccl(gfq_handle* h, void* comm, void* summary_out, void* stream) {
+    if (!h || !h->launched || !comm) return set_err(GFQ_EINVAL, "gfq_reduce_nccl: no launched batch or no communicator");
+    int rc = nccl_load();
+    if (rc) return rc;
+    CK(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    NK(g_nccl.group_start());
+    if (h->out_n[GFQ_OUT_HIST] > 0)
+        NK(g_nccl.all_reduce(h->out[GFQ_OUT_HIST].p, h->out[GFQ_OUT_HIST].p, (size_t)h->out_n[GFQ_OUT_HIST],
+                             NCCL_UINT64, NCCL_SUM, comm, st));
+    if (summary_out && h->n_sims > 0)
+        NK(g_nccl.all_gather(h->out[GFQ_OUT_SUMMARY].p, summary_out, (size_t)3 * h->n_sims, NCCL_FLOAT64,
+                             comm, st));
+    NK(g_nccl.group_end());
     return GFQ_OK;
 }
 

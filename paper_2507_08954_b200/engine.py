@@ -262,6 +262,16 @@ class Engine:
         return {"launches_per_step": int(v[0]), "cta_threads": int(v[1]),
                 "flows_global": bool(v[2]), "warps_per_block": int(v[3]), "ctas": int(v[4])}
 
+    def reduce_nccl(self, comm: "NcclComm", summary_out=None, stream=None) -> None:
+        """gfq_reduce_nccl: sum the last launch's latency histograms over every
+        rank of `comm` (in place) and gather the per-simulation summary rows
+        into `summary_out` (a CUDA tensor of n_ranks * n_sims * 3 float64, or
+        None).  Enqueued on `stream` after the launch."""
+        ptr = None
+        if summary_out is not None:
+            ptr = C.c_void_p(summary_out.data_ptr())
+        check(self._L.gfq_reduce_nccl(self._h, comm.handle, ptr, _stream_handle(stream)))
+
     def kernel_times(self, cap: int = 256):
         """(sim_ms, reduce_ms) arrays of the launches since the last call."""
         a = np.zeros(cap, dtype=np.float32)
@@ -314,6 +324,29 @@ class Engine:
     @property
     def rec_off(self):
         return self._rec_off
+
+
+class NcclComm:
+    """An NCCL communicator made through libgfq (gfq_nccl_comm_init), one
+    rank per GPU; rank 0 makes the id (unique_id()) and shares it (e.g. with
+    torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, n_ranks: int, rank: int, uid: bytes):
+        self._L = lib()
+        h = C.c_void_p()
+        check(self._L.gfq_nccl_comm_init(C.byref(h), int(n_ranks), bytes(uid), int(rank)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().gfq_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            check(self._L.gfq_nccl_comm_destroy(self.handle))
+            self.handle = None
 
 
 @dataclass
