@@ -38,6 +38,8 @@ CLI_COMMANDS = [
     ("run_small_naive", ["run", "--config", "small.cfg", "--policy", "fcfs_naive"]),
     ("run_small_seed", ["run", "--config", "small.cfg", "--seed", "11"]),
     ("run_twodev", ["run", "--config", "twodev.cfg"]),
+    ("compare_files", ["compare", "--config", "files.cfg", "--policies", "mqfq,fcfs,batch,sjf"]),
+    ("sweep_files_T", ["sweep", "--config", "files.cfg", "--param", "T", "--values", "0,2,8"]),
 ]
 
 
