@@ -42,7 +42,8 @@
 namespace gfq {
 
 // ----------------------------------------------------------------------------
-// stats reducer (runs in the same warp after the event loop)
+// stats reducer
+enum { RED_FLOW_BYTES = 24 };   // per-flow reducer scratch: naive f64 + cnt, cur, first/order i32
 //
 // Per function, in completion order (metrics.py:195-220):
 //   count, mean = sum(lat)/n (builtin Neumaier sum), var = sum((x-mean)**2)/(n-1),
@@ -50,24 +51,25 @@ namespace gfq {
 // weighted_avg_latency (metrics.py:63-77): per-function naive sums in a dict
 // ordered by first completion, then sum(n*(s/n)) / total;
 // cold_hit_rate (metrics.py:80-84); mean_util (metrics.py:223-226).
-// Lane (f mod 32) owns function f; the completion stream is read 32 records
-// at a time (coalesced) and replayed in order through shuffles.
-__device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base, int lane, int sid) {
+//
+// One warp per simulation.  The completion stream is grouped by function
+// with a stable counting sort (coalesced 32-record batches, __match_any_sync
+// ranks), so each lane then walks its own functions' latencies in
+// completion order -- every sum is the reference's sequential one, but the
+// lanes run their functions in parallel instead of replaying every record
+// through the whole warp.  Scratch: 24 B per flow (shared memory or global)
+// and 8 B per record (global, `rec`).
+__device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base, double* rec, int lane, int sid) {
     const gfq_sim* sim = p.sims + sid;
     const int nf = p.trace_nf[sim->trace];
     const int nrec = (int)p.counters[(int64_t)sid * GFQ_NCOUNTERS + C_DISP];
     const int64_t roff = p.sim_roff[sid], tb = p.tab_off[sim->flowtab];
     const int F = p.L.F;
-    // per-warp scratch: sum/sumc = latency sum + Neumaier compensation
-    // (then mean), naive = naive sum, var/varc = (x-mean)^2 sum + compensation,
-    // cnt = count, cold = cold count, first = first-completion rank,
-    // order = rank -> flow, vcnt = variance-pass count
-    double *sum = (double*)base, *sumc = sum + F, *naive = sum + 2 * F, *var = sum + 3 * F, *varc = sum + 4 * F;
-    int *cnt = (int*)(sum + 5 * F), *coldc = cnt + F, *first = cnt + 2 * F, *order = cnt + 3 * F, *vcnt = cnt + 4 * F;
-    for (int f = lane; f < nf; f += 32) {
-        sum[f] = 0.0; sumc[f] = 0.0; naive[f] = 0.0; var[f] = 0.0; varc[f] = 0.0;
-        cnt[f] = 0; coldc[f] = 0; first[f] = -1; vcnt[f] = 0;
-    }
+    // per flow: naive sum, record count, end cursor of its group, first
+    // completion index (then: rank -> flow order)
+    double* naive = (double*)base;
+    int *cnt = (int*)(naive + F), *cur = cnt + F, *first = cnt + 2 * F, *order = cnt + 3 * F;
+    for (int f = lane; f < nf; f += 32) { naive[f] = 0.0; cnt[f] = 0; first[f] = 0x7fffffff; }
     __syncwarp();
     // completion stream: completion time, trace position, flow | cold << 31;
     // latency = complete - arrival (InvocationRecord.latency_s)
@@ -75,96 +77,125 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
     const int32_t* cpos = p.comp_pos + roff;
     const double* arrival = p.arrival + p.trace_off[sim->trace];
     const int32_t* meta = p.comp_meta + roff;
-    int nfirst = 0;
     int colds = 0;
     const bool want_hist = (p.outputs & GFQ_WANT_HIST) && sim->group >= 0;
     const double hl0 = want_hist ? log(p.hist_lo) : 0.0;
     const double hscale = want_hist ? (double)p.hist_bins / (log(p.hist_hi) - hl0) : 0.0;
     const int32_t* hrow = p.hist_row + tb;
-    for (int base = 0; base < nrec; base += 32) {
-        int k = base + lane;
+    // pass 1: histograms, per-function counts and first completions
+    for (int b0 = 0; b0 < nrec; b0 += 32) {
+        const int k = b0 + lane;
+        const bool in = k < nrec;
         double x = 0.0; int32_t m = 0;
-        if (k < nrec) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
-        if (want_hist && k < nrec) {
-            int fn = m & 0x7fffffff;
+        if (in) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
+        const int fn = m & 0x7fffffff;
+        if (want_hist && in) {
             int b = x > 0.0 ? (int)floor((log(x) - hl0) * hscale) : 0;
             b = max(0, min(p.hist_bins - 1, b));
             int64_t o = ((int64_t)sim->group * p.hist_rows + hrow[fn]) * p.hist_bins + b;
             atomicAdd(&p.hist[o], 1ull);
         }
-        int nb = min(32, nrec - base);
-        for (int j = 0; j < nb; j++) {
-            double xj = __shfl_sync(FULLMASK, x, j);
-            int32_t mj = __shfl_sync(FULLMASK, m, j);
-            int fn = mj & 0x7fffffff;
-            bool cold = mj < 0;
-            bool isfirst = false;
-            if ((fn & 31) == lane) {
-                int c = cnt[fn];
-                if (c == 0) { isfirst = true; sum[fn] = 0.0 + xj; first[fn] = nfirst; }
-                else {
-                    double sf = sum[fn];
-                    double t = sf + xj;
-                    if (fabs(sf) >= fabs(xj)) sumc[fn] += (sf - t) + xj;
-                    else                      sumc[fn] += (xj - t) + sf;
-                    sum[fn] = t;
-                }
-                naive[fn] = naive[fn] + xj;
-                cnt[fn] = c + 1;
-                if (cold) coldc[fn] += 1;
-            }
-            if (__ballot_sync(FULLMASK, isfirst)) nfirst++;
-            colds += cold ? 1 : 0;
+        if (in) { atomicAdd(&cnt[fn], 1); atomicMin(&first[fn], k); }
+        colds += __popc(__ballot_sync(FULLMASK, in && m < 0));
+    }
+    __syncwarp();
+    // group starts (exclusive prefix of the counts, 32 flows per step)
+    int carry = 0;
+    for (int f0 = 0; f0 < nf; f0 += 32) {
+        const int f = f0 + lane;
+        const int c = f < nf ? cnt[f] : 0;
+        int inc = c;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(FULLMASK, inc, d);
+            if (lane >= d) inc += y;
         }
+        if (f < nf) cur[f] = carry + inc - c;
+        carry += __shfl_sync(FULLMASK, inc, 31);
     }
     __syncwarp();
-    // means, then the second (variance) pass
-    for (int f = lane; f < nf; f += 32) {
-        int c = cnt[f];
-        double sv = sum[f], sc = sumc[f];
-        double s = (c == 0) ? 0.0 : ((sc != 0.0 && isfinite(sc)) ? sv + sc : sv);
-        sum[f] = c ? s / (double)c : 0.0;                      // mean
-        if (first[f] >= 0) order[first[f]] = f;
-    }
-    __syncwarp();
-    for (int base = 0; base < nrec; base += 32) {
-        int k = base + lane;
+    // pass 2: stable scatter by function; cold is carried in the sign bit
+    // (latencies are >= 0, so -x with x == 0 is -0.0 and still decodes)
+    for (int b0 = 0; b0 < nrec; b0 += 32) {
+        const int k = b0 + lane;
+        const bool in = k < nrec;
         double x = 0.0; int32_t m = 0;
-        if (k < nrec) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
-        int nb = min(32, nrec - base);
-        for (int j = 0; j < nb; j++) {
-            double xj = __shfl_sync(FULLMASK, x, j);
-            int fn = __shfl_sync(FULLMASK, m, j) & 0x7fffffff;
-            if ((fn & 31) == lane) {
-                double dx = xj - sum[fn];
-                double v = dx * dx;                      // (x - mean) ** 2
-                int c = vcnt[fn];
-                if (c == 0) { var[fn] = 0.0 + v; }
-                else {
-                    double sf = var[fn];
-                    double t = sf + v;
-                    if (fabs(sf) >= fabs(v)) varc[fn] += (sf - t) + v;
-                    else                     varc[fn] += (v - t) + sf;
-                    var[fn] = t;
-                }
-                vcnt[fn] = c + 1;
+        if (in) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
+        const int fn = in ? (m & 0x7fffffff) : -1;
+        const unsigned peers = __match_any_sync(FULLMASK, fn);
+        if (in) {
+            const int pos = cur[fn] + __popc(peers & ((1u << lane) - 1));
+            rec[pos] = m < 0 ? -x : x;
+        }
+        __syncwarp();
+        if (in && lane == 31 - __clz(peers)) cur[fn] += __popc(peers);
+        __syncwarp();
+    }
+    // pass 3: each lane walks its functions' latencies in completion order
+    const int64_t fo = p.sim_foff[sid];
+    for (int f = lane; f < nf; f += 32) {
+        const int c = cnt[f];
+        if (c == 0) {
+            if (p.outputs & GFQ_WANT_STATS) { p.f_count[fo + f] = 0; p.f_mean[fo + f] = 0.0; p.f_var[fo + f] = 0.0; p.f_cold[fo + f] = 0.0; }
+            continue;
+        }
+        const int s0 = cur[f] - c;
+        double sv = 0.0, sc = 0.0, nv = 0.0;
+        int cc = 0;
+        for (int j = 0; j < c; j++) {
+            const double v = rec[s0 + j];
+            const double x = fabs(v);
+            cc += signbit(v) ? 1 : 0;
+            if (j == 0) sv = 0.0 + x;
+            else {
+                const double t = sv + x;
+                if (fabs(sv) >= fabs(x)) sc += (sv - t) + x;
+                else                     sc += (x - t) + sv;
+                sv = t;
             }
+            nv = nv + x;
+        }
+        const double s = (sc != 0.0 && isfinite(sc)) ? sv + sc : sv;
+        const double mean = s / (double)c;
+        double vf = 0.0, vc = 0.0;
+        for (int j = 0; j < c; j++) {
+            const double dx = fabs(rec[s0 + j]) - mean;
+            const double v = dx * dx;                        // (x - mean) ** 2
+            if (j == 0) vf = 0.0 + v;
+            else {
+                const double t = vf + v;
+                if (fabs(vf) >= fabs(v)) vc += (vf - t) + v;
+                else                     vc += (v - t) + vf;
+                vf = t;
+            }
+        }
+        const double vs = (vc != 0.0 && isfinite(vc)) ? vf + vc : vf;
+        naive[f] = nv;
+        if (p.outputs & GFQ_WANT_STATS) {
+            p.f_count[fo + f] = c;
+            p.f_mean[fo + f] = mean;
+            p.f_var[fo + f] = c > 1 ? vs / (double)(c - 1) : 0.0;
+            p.f_cold[fo + f] = 100.0 * (double)cc / (double)c;
         }
     }
     __syncwarp();
-    const int64_t fo = p.sim_foff[sid];
-    if (p.outputs & GFQ_WANT_STATS) {
-        for (int f = lane; f < nf; f += 32) {
-            int c = cnt[f];
-            double vf = var[f], vc = varc[f];
-            double vs = (c == 0) ? 0.0 : ((vc != 0.0 && isfinite(vc)) ? vf + vc : vf);
-            p.f_count[fo + f] = c;
-            p.f_mean[fo + f] = sum[f];
-            p.f_var[fo + f] = c > 1 ? vs / (double)(c - 1) : 0.0;
-            p.f_cold[fo + f] = c ? 100.0 * (double)coldc[f] / (double)c : 0.0;
-        }
+    // weighted_avg_latency: builtin sum over functions in first-completion
+    // order.  The record scratch is free again: mark each function at its
+    // first completion index, then read the marks in order.
+    int* mark = (int*)rec;
+    for (int k = lane; k < nrec; k += 32) mark[k] = -1;
+    __syncwarp();
+    for (int f = lane; f < nf; f += 32) if (cnt[f] > 0) mark[first[f]] = f;
+    __syncwarp();
+    int nfirst = 0;
+    for (int b0 = 0; b0 < nrec; b0 += 32) {
+        const int k = b0 + lane;
+        const int f = k < nrec ? mark[k] : -1;
+        const unsigned hit = __ballot_sync(FULLMASK, f >= 0);
+        if (f >= 0) order[nfirst + __popc(hit & ((1u << lane) - 1))] = f;
+        nfirst += __popc(hit);
     }
-    // weighted_avg_latency: builtin sum over functions in first-completion order
+    __syncwarp();
     PySum num; ps_init(num);
     for (int r = 0; r < nfirst; r++) {
         int f = order[r];
@@ -392,11 +423,12 @@ __global__ void __launch_bounds__(128) k_reduce(const __grid_constant__ Params p
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
-    const size_t scratch = (size_t)60 * p.L.F;
+    const size_t scratch = (size_t)RED_FLOW_BYTES * p.L.F;
     unsigned char* base = FG ? p.gscratch + (size_t)(blockIdx.x * wpb + warp) * scratch
                              : smem + (size_t)warp * scratch;
+    double* rec = p.rscratch + (size_t)(blockIdx.x * wpb + warp) * p.rscratch_per_warp;
     for (int sid = blockIdx.x * wpb + warp; sid < p.n_sims; sid += gridDim.x * wpb)
-        if (p.status[sid] == GFQ_SIM_OK) reduce_one(p, base, lane, sid);
+        if (p.status[sid] == GFQ_SIM_OK) reduce_one(p, base, rec, lane, sid);
 }
 
 // Trace loader: one warp per trace.  Counting sort of trace positions by
@@ -533,7 +565,8 @@ struct gfq_handle {
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
     int32_t out_b[GFQ_OUT_COUNT_] = {0};
-    DBuf comp_lat, comp_meta, comp_pos, gscratch, fscratch;
+    DBuf comp_lat, comp_meta, comp_pos, gscratch, fscratch, rscr;
+    int64_t rscr_per_warp = 1;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     // kernel classes run concurrently on side streams (fork/join on the
     // caller's stream), so one class's tail overlaps the next class's start
@@ -589,7 +622,7 @@ int gfq_create(int device, gfq_handle** out) {
 int gfq_destroy(gfq_handle* h) {
     if (!h) return GFQ_OK;
     cudaSetDevice(h->device);
-    DBuf* all[] = {&h->gscratch, &h->fscratch, &h->comp_pos, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
+    DBuf* all[] = {&h->gscratch, &h->fscratch, &h->rscr, &h->comp_pos, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
                    &h->fpos, &h->warm, &h->cold, &h->mem, &h->share, &h->weight, &h->hist_row,
                    &h->tab_off, &h->dcfg, &h->execs, &h->sims, &h->order, &h->sim_foff,
                    &h->sim_roff, &h->work, &h->comp_lat, &h->comp_meta};
@@ -1041,16 +1074,17 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     }
     // reducer: 60 B of scratch per flow per warp, shared memory or global
     int rwpb = 4;
-    const bool rglobal = L.flows_global || (size_t)60 * L.F > h->smem_optin;
-    if (!rglobal) while (rwpb > 1 && (size_t)rwpb * 60 * L.F > h->smem_optin) rwpb--;
+    const bool rglobal = L.flows_global || (size_t)RED_FLOW_BYTES * L.F > h->smem_optin;
+    if (!rglobal) while (rwpb > 1 && (size_t)rwpb * RED_FLOW_BYTES * L.F > h->smem_optin) rwpb--;
     int rblocks = std::max(1, std::min((n_sims + rwpb - 1) / rwpb, 8 * h->n_sm));
     if (!rglobal)
         CK(cudaFuncSetAttribute(k_reduce<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(rwpb * 60 * L.F)));
+                                (int)(rwpb * RED_FLOW_BYTES * L.F)));
     size_t gscr = 0;
     if (L.flows_global)
         for (int k = 0; k < NCLASS; k++) gscr = std::max(gscr, (size_t)cblocks[k] * (k == CLASS_CTA ? 1 : wpb) * L.fe_bytes);
-    if (rglobal) gscr = std::max(gscr, (size_t)rblocks * rwpb * 60 * L.F);
+    if (rglobal) gscr = std::max(gscr, (size_t)rblocks * rwpb * RED_FLOW_BYTES * L.F);
+    const int64_t rper = std::max(max_n, 1);              // reducer record scratch per warp
 
     int rc;
     if ((rc = h->sims.ensure(sizeof(gfq_sim) * std::max(n_sims, 1))) || (rc = h->order.ensure(4 * std::max(n_sims, 1))) ||
@@ -1058,7 +1092,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         (rc = h->work.ensure(4 * NCLASS)) || (rc = h->comp_lat.ensure(8 * std::max<int64_t>(recs, 1))) ||
         (rc = h->comp_meta.ensure(4 * std::max<int64_t>(recs, 1))) ||
         (gscr && (rc = h->gscratch.ensure(gscr))) ||
-        (rc = h->comp_pos.ensure(4 * std::max<int64_t>(recs, 1))))
+        (rc = h->comp_pos.ensure(4 * std::max<int64_t>(recs, 1))) ||
+        (rc = h->rscr.ensure((size_t)8 * rblocks * rwpb * rper)))
         return rc;
     for (int id = 0; id < GFQ_OUT_COUNT_; id++) h->out_n[id] = 0;
     if ((rc = alloc_out(h, GFQ_OUT_STATUS, n_sims)) || (rc = alloc_out(h, GFQ_OUT_COUNTERS, (int64_t)GFQ_NCOUNTERS * n_sims)) ||
@@ -1121,6 +1156,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->rwpb = rwpb;
     h->rblocks = rblocks;
     h->rglobal = rglobal;
+    h->rscr_per_warp = rper;
     for (int k = 0; k < NCLASS; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; }
     h->prepared = true;
     h->launched = false;
@@ -1159,6 +1195,7 @@ static Params make_params(gfq_handle* h) {
     p.f_cold = h->out[GFQ_OUT_FLOW_COLD_PCT].as<double>();
     p.comp_lat = h->comp_lat.as<double>(); p.comp_meta = h->comp_meta.as<int32_t>();
     p.comp_pos = h->comp_pos.as<int32_t>();
+    p.rscratch = h->rscr.as<double>(); p.rscratch_per_warp = h->rscr_per_warp;
     p.rec_dispatch = h->out[GFQ_OUT_REC_DISPATCH].as<double>();
     p.rec_complete = h->out[GFQ_OUT_REC_COMPLETE].as<double>();
     p.rec_pure = h->out[GFQ_OUT_REC_PURE].as<double>();
@@ -1244,7 +1281,7 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(re[1], st));
     if (h->n_sims > 0) {
         if (h->rglobal) k_reduce<true><<<h->rblocks, h->rwpb * 32, 0, st>>>(p);
-        else k_reduce<false><<<h->rblocks, h->rwpb * 32, (size_t)h->rwpb * 60 * h->L.F, st>>>(p);
+        else k_reduce<false><<<h->rblocks, h->rwpb * 32, (size_t)h->rwpb * RED_FLOW_BYTES * h->L.F, st>>>(p);
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(h->ev[2], st));

@@ -128,6 +128,8 @@ struct Params {
     double* event_time; int64_t* event_meta; int64_t* event_count; int64_t event_log_cap;
     unsigned long long* hist; int32_t hist_rows, hist_bins; double hist_lo, hist_hi;
     int32_t* work;                 // work-queue counter
+    double* rscratch;              // reducer: per-warp record scratch (rscratch_per_warp doubles)
+    int64_t rscratch_per_warp;
     int32_t cta_min;               // CTA mode: scans shorter than this stay on the leader warp
     unsigned char* gscratch;       // per-warp fe slices when L.flows_global
 };
