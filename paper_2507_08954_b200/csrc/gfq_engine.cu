@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -919,30 +920,31 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     gfq_launch_cfg c = *cfg;
     if (c.outputs & GFQ_WANT_DISPATCH) c.outputs |= GFQ_WANT_RECORDS;   // rows read dispatch_s
     int max_nf = 1, nd = 1, P = 1, R = 1, S = 4, max_n = 0;
+    std::unordered_map<int64_t, double> maxmem;
     int64_t flows = 0, recs = 0;
     std::vector<int64_t> foffs(n_sims + 1, 0), roffs(n_sims + 1, 0);
     std::vector<double> cost(n_sims);
     for (int i = 0; i < n_sims; i++) {
         const gfq_sim& s = sims[i];
-        std::string who = "sim " + std::to_string(i) + ": ";
-        if (s.trace < 0 || s.trace >= h->n_traces) return set_err(GFQ_EINVAL, who + "trace id out of range");
-        if (s.flowtab < 0 || s.flowtab >= h->n_tabs) return set_err(GFQ_EINVAL, who + "flow table id out of range");
-        if (s.policy < 0 || s.policy > GFQ_POLICY_FCFS_NAIVE) return set_err(GFQ_EINVAL, who + "unknown policy");
-        if (!(s.t_overrun >= 0)) return set_err(GFQ_EINVAL, who + "t_overrun must be >= 0");
+        auto who = [i]() { return "sim " + std::to_string(i) + ": "; };   // built only on error
+        if (s.trace < 0 || s.trace >= h->n_traces) return set_err(GFQ_EINVAL, who() + "trace id out of range");
+        if (s.flowtab < 0 || s.flowtab >= h->n_tabs) return set_err(GFQ_EINVAL, who() + "flow table id out of range");
+        if (s.policy < 0 || s.policy > GFQ_POLICY_FCFS_NAIVE) return set_err(GFQ_EINVAL, who() + "unknown policy");
+        if (!(s.t_overrun >= 0)) return set_err(GFQ_EINVAL, who() + "t_overrun must be >= 0");
         if (!(s.alpha >= 0)) return set_err(GFQ_EINVAL, "alpha must be >= 0");
         int nf = h->h_trace_nf[s.trace];
         int64_t n = h->h_trace_off[s.trace + 1] - h->h_trace_off[s.trace];
         int64_t tabn = h->h_tab_off[s.flowtab + 1] - h->h_tab_off[s.flowtab];
-        if (tabn < nf) return set_err(GFQ_EINVAL, who + "flow table shorter than the trace's flow set");
+        if (tabn < nf) return set_err(GFQ_EINVAL, who() + "flow table shorter than the trace's flow set");
         if (s.device_model == GFQ_DEVMODEL_SCRIPTED) {
             if (s.scripted_d < 1 || s.exec_len < 1 || s.exec_off < 0 || s.exec_off + s.exec_len > h->n_execs)
-                return set_err(GFQ_EINVAL, who + "bad scripted-device parameters");
+                return set_err(GFQ_EINVAL, who() + "bad scripted-device parameters");
             R = std::max(R, s.scripted_d);
         } else if (s.device_model == GFQ_DEVMODEL_DEVICESET) {
             if (s.n_devices < 1 || s.n_devices > GFQ_MAX_DEVICES)
-                return set_err(GFQ_EINVAL, who + "n_devices must be in [1, 8]");
+                return set_err(GFQ_EINVAL, who() + "n_devices must be in [1, 8]");
             if (s.device_cfg < 0 || s.device_cfg + s.n_devices > (int)h->h_dcfg.size())
-                return set_err(GFQ_EINVAL, who + "device config range out of bounds");
+                return set_err(GFQ_EINVAL, who() + "device config range out of bounds");
             nd = std::max(nd, s.n_devices);
             double period = h->h_dcfg[s.device_cfg].monitor_period_s;
             for (int d = 0; d < s.n_devices; d++) period = std::min(period, h->h_dcfg[s.device_cfg + d].monitor_period_s);
@@ -952,12 +954,20 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
                 R = std::max(R, dc.d_max);
                 if (dc.pool_enabled) P = std::max(P, dc.pool_max_containers + 1);
                 S = std::max(S, (int)ceil(dc.util_window_s / period) + 3);
-                for (int f = 0; f < nf; f++)    // the reference never terminates otherwise
-                    if (h->h_mem[tb + f] > dc.mem_capacity_mb)
-                        return set_err(GFQ_EINVAL, who + "a function's mem_mb exceeds the device's mem_capacity_mb");
+                // the reference never terminates otherwise; the
+                // table's max over the trace's flows is computed once per (table, nf)
+                const int64_t mk = ((int64_t)s.flowtab << 20) | nf;
+                auto it = maxmem.find(mk);
+                if (it == maxmem.end()) {
+                    double m = -INFINITY;
+                    for (int f = 0; f < nf; f++) m = std::max(m, h->h_mem[tb + f]);
+                    it = maxmem.emplace(mk, m).first;
+                }
+                if (it->second > dc.mem_capacity_mb)
+                    return set_err(GFQ_EINVAL, who() + "a function's mem_mb exceeds the device's mem_capacity_mb");
             }
         } else {
-            return set_err(GFQ_EINVAL, who + "unknown device model");
+            return set_err(GFQ_EINVAL, who() + "unknown device model");
         }
         max_nf = std::max(max_nf, nf);
         max_n = std::max<int>(max_n, (int)n);
