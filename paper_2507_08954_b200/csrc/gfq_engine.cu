@@ -44,7 +44,8 @@ namespace gfq {
 
 // ----------------------------------------------------------------------------
 // stats reducer
-enum { RED_FLOW_BYTES = 24 };   // per-flow reducer scratch: naive f64 + cnt, cur, first/order i32
+enum { RED_FLOW_BYTES = 24,     // per-flow reducer scratch: naive f64 + cnt, cur, first/order i32
+       RED_CHUNK = 8 };         // records a reducer lane loads ahead
 //
 // Per function, in completion order (metrics.py:195-220):
 //   count, mean = sum(lat)/n (builtin Neumaier sum), var = sum((x-mean)**2)/(n-1),
@@ -90,11 +91,20 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
         double x = 0.0; int32_t m = 0;
         if (in) { x = ctime[k] - __ldg(arrival + cpos[k]); m = meta[k]; }
         const int fn = m & 0x7fffffff;
-        if (want_hist && in) {
-            int b = x > 0.0 ? (int)floor((log(x) - hl0) * hscale) : 0;
-            b = max(0, min(p.hist_bins - 1, b));
-            int64_t o = ((int64_t)sim->group * p.hist_rows + hrow[fn]) * p.hist_bins + b;
-            atomicAdd(&p.hist[o], 1ull);
+        if (want_hist) {
+            // warp-aggregated: one atomic per distinct (row, bin) of the batch
+            // (a sweep's simulations all hit the same few popular bins)
+            int key = -1;
+            if (in) {
+                int b = x > 0.0 ? (int)floor((log(x) - hl0) * hscale) : 0;
+                b = max(0, min(p.hist_bins - 1, b));
+                key = hrow[fn] * p.hist_bins + b;
+            }
+            const unsigned peers = __match_any_sync(FULLMASK, key);
+            if (in && lane == __ffs(peers) - 1) {
+                int64_t o = (int64_t)sim->group * p.hist_rows * p.hist_bins + key;
+                atomicAdd(&p.hist[o], (unsigned long long)__popc(peers));
+            }
         }
         if (in) { atomicAdd(&cnt[fn], 1); atomicMin(&first[fn], k); }
         colds += __popc(__ballot_sync(FULLMASK, in && m < 0));
@@ -141,33 +151,48 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
             continue;
         }
         const int s0 = cur[f] - c;
+        // the walks load RED_CHUNK records at a time (independent loads in
+        // flight), then accumulate them in order
         double sv = 0.0, sc = 0.0, nv = 0.0;
         int cc = 0;
-        for (int j = 0; j < c; j++) {
-            const double v = rec[s0 + j];
-            const double x = fabs(v);
-            cc += signbit(v) ? 1 : 0;
-            if (j == 0) sv = 0.0 + x;
-            else {
-                const double t = sv + x;
-                if (fabs(sv) >= fabs(x)) sc += (sv - t) + x;
-                else                     sc += (x - t) + sv;
-                sv = t;
+        for (int j0 = 0; j0 < c; j0 += RED_CHUNK) {
+            double vb[RED_CHUNK];
+            #pragma unroll
+            for (int u = 0; u < RED_CHUNK; u++) vb[u] = j0 + u < c ? rec[s0 + j0 + u] : 0.0;
+            #pragma unroll
+            for (int u = 0; u < RED_CHUNK; u++) {
+                if (j0 + u >= c) break;
+                const double x = fabs(vb[u]);
+                cc += signbit(vb[u]) ? 1 : 0;
+                if (j0 + u == 0) sv = 0.0 + x;
+                else {
+                    const double t = sv + x;
+                    if (fabs(sv) >= fabs(x)) sc += (sv - t) + x;
+                    else                     sc += (x - t) + sv;
+                    sv = t;
+                }
+                nv = nv + x;
             }
-            nv = nv + x;
         }
         const double s = (sc != 0.0 && isfinite(sc)) ? sv + sc : sv;
         const double mean = s / (double)c;
         double vf = 0.0, vc = 0.0;
-        for (int j = 0; j < c; j++) {
-            const double dx = fabs(rec[s0 + j]) - mean;
-            const double v = dx * dx;                        // (x - mean) ** 2
-            if (j == 0) vf = 0.0 + v;
-            else {
-                const double t = vf + v;
-                if (fabs(vf) >= fabs(v)) vc += (vf - t) + v;
-                else                     vc += (v - t) + vf;
-                vf = t;
+        for (int j0 = 0; j0 < c; j0 += RED_CHUNK) {
+            double vb[RED_CHUNK];
+            #pragma unroll
+            for (int u = 0; u < RED_CHUNK; u++) vb[u] = j0 + u < c ? rec[s0 + j0 + u] : 0.0;
+            #pragma unroll
+            for (int u = 0; u < RED_CHUNK; u++) {
+                if (j0 + u >= c) break;
+                const double dx = fabs(vb[u]) - mean;
+                const double v = dx * dx;                    // (x - mean) ** 2
+                if (j0 + u == 0) vf = 0.0 + v;
+                else {
+                    const double t = vf + v;
+                    if (fabs(vf) >= fabs(v)) vc += (vf - t) + v;
+                    else                     vc += (v - t) + vf;
+                    vf = t;
+                }
             }
         }
         const double vs = (vc != 0.0 && isfinite(vc)) ? vf + vc : vf;
@@ -1086,7 +1111,16 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     int rwpb = 4;
     const bool rglobal = L.flows_global || (size_t)RED_FLOW_BYTES * L.F > h->smem_optin;
     if (!rglobal) while (rwpb > 1 && (size_t)rwpb * RED_FLOW_BYTES * L.F > h->smem_optin) rwpb--;
-    int rblocks = std::max(1, std::min((n_sims + rwpb - 1) / rwpb, 8 * h->n_sm));
+    int red_per_sm = 8;
+    if (!rglobal) {
+        CK(cudaFuncSetAttribute(k_reduce<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(rwpb * RED_FLOW_BYTES * L.F)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&red_per_sm, k_reduce<false>, rwpb * 32,
+                                                         (size_t)rwpb * RED_FLOW_BYTES * L.F));
+    } else {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&red_per_sm, k_reduce<true>, rwpb * 32, 0));
+    }
+    int rblocks = std::max(1, std::min((n_sims + rwpb - 1) / rwpb, std::max(red_per_sm, 1) * h->n_sm));
     if (!rglobal)
         CK(cudaFuncSetAttribute(k_reduce<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(rwpb * RED_FLOW_BYTES * L.F)));

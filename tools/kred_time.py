@@ -3,7 +3,7 @@ import numpy as np
 from paper_2507_08954_b200 import _abi, sweep
 from paper_2507_08954_b200.engine import Engine
 eng = Engine(0)
-w = sweep.build('c3', 0, engine=eng)
+w = sweep.build(sys.argv[1] if len(sys.argv) > 1 else 'c3', 0, engine=eng)
 w.upload(eng)
 for outs, name in ((_abi.WANT_STATS | _abi.WANT_HIST, 'stats+hist'), (_abi.WANT_STATS, 'stats')):
     kw = dict(hist_groups=w.groups, hist_rows=w.hist_rows, hist_bins=sweep.HIST_BINS, hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S) if outs & _abi.WANT_HIST else {}
