@@ -457,6 +457,27 @@ __global__ void __launch_bounds__(128) k_reduce(const __grid_constant__ Params p
         if (p.status[sid] == GFQ_SIM_OK) reduce_one(p, base, rec, lane, sid);
 }
 
+// Trace validation (Simulation.__init__, engine.py:50-52,72-73), one block
+// per trace: the smallest (trace, position, check) failure wins (atomicMin on
+// trace << 29 | position << 2 | check; checks: 0 flow id out of range,
+// 1 decreasing time, 2 non-finite or negative time -- a sequential scan's order).
+__global__ void k_validate_traces(const double* arrival, const int32_t* flow, const int64_t* trace_off,
+                                  const int32_t* trace_nf, unsigned long long* err) {
+    const int t = blockIdx.x;
+    const int64_t a = trace_off[t], b = trace_off[t + 1];
+    const int nf = trace_nf[t];
+    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        int kind = -1;
+        const int f = flow[i];
+        const double x = arrival[i];
+        if (f < 0 || f >= nf) kind = 0;
+        else if (i > a && x < arrival[i - 1]) kind = 1;
+        else if (!(x >= 0.0) || !isfinite(x)) kind = 2;
+        if (kind >= 0)
+            atomicMin(err, ((unsigned long long)t << 29) | ((unsigned long long)(i - a) << 2) | (unsigned)kind);
+    }
+}
+
 // Trace loader: one warp per trace.  Counting sort of trace positions by
 // flow rank, stable (arrival order kept within a flow) via __match_any_sync.
 __global__ void k_trace_index(const int32_t* flow, const int64_t* trace_off, const int32_t* trace_nf,
@@ -591,7 +612,7 @@ struct gfq_handle {
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
     int32_t out_b[GFQ_OUT_COUNT_] = {0};
-    DBuf comp_lat, comp_meta, comp_pos, gscratch, fscratch, rscr;
+    DBuf comp_lat, comp_meta, comp_pos, gscratch, fscratch, rscr, verr;
     int64_t rscr_per_warp = 1;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     // kernel classes run concurrently on side streams (fork/join on the
@@ -648,7 +669,7 @@ int gfq_create(int device, gfq_handle** out) {
 int gfq_destroy(gfq_handle* h) {
     if (!h) return GFQ_OK;
     cudaSetDevice(h->device);
-    DBuf* all[] = {&h->gscratch, &h->fscratch, &h->rscr, &h->comp_pos, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
+    DBuf* all[] = {&h->gscratch, &h->fscratch, &h->rscr, &h->verr, &h->comp_pos, &h->arrival, &h->flow, &h->trace_off, &h->trace_nf, &h->foff_off, &h->foff,
                    &h->fpos, &h->warm, &h->cold, &h->mem, &h->share, &h->weight, &h->hist_row,
                    &h->tab_off, &h->dcfg, &h->execs, &h->sims, &h->order, &h->sim_foff,
                    &h->sim_roff, &h->work, &h->comp_lat, &h->comp_meta};
@@ -681,15 +702,6 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
         if (b - a >= (1 << 27)) return set_err(GFQ_EINVAL, "gfq_upload_traces: trace longer than 2^27 arrivals");
         if (n_flows[t] < 0 || n_flows[t] > 0xffff)
             return set_err(GFQ_EINVAL, "gfq_upload_traces: n_flows out of range");
-        for (int64_t i = a; i < b; i++) {
-            if (flow[i] < 0 || flow[i] >= n_flows[t])
-                return set_err(GFQ_EINVAL, "gfq_upload_traces: flow id out of range in trace " + std::to_string(t));
-            if (i > a && arrival[i] < arrival[i - 1])   // engine.py:72-73
-                return set_err(GFQ_EINVAL, "trace arrival times must be non-decreasing (trace " +
-                                               std::to_string(t) + ")");
-            if (!(arrival[i] >= 0.0) || !isfinite(arrival[i]))
-                return set_err(GFQ_EINVAL, "gfq_upload_traces: arrival times must be finite and >= 0");
-        }
         foff_off[t + 1] = foff_off[t] + n_flows[t] + 1;
         max_nf = std::max(max_nf, n_flows[t]);
     }
@@ -708,6 +720,25 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
     }
     CK(cudaMemcpy(h->trace_off.p, off, 8 * (n_traces + 1), cudaMemcpyHostToDevice));
     if (n_traces) CK(cudaMemcpy(h->trace_nf.p, n_flows, 4 * n_traces, cudaMemcpyHostToDevice));
+    // per-arrival validation (engine.py:50-52,72-73) on the GPU; the first
+    // failure in (trace, position, check) order is the one reported, as a
+    // sequential scan would.  On failure no traces stay resident.
+    if (total) {
+        if ((rc = h->verr.ensure(8))) return rc;
+        CK(cudaMemset(h->verr.p, 0xff, 8));
+        k_validate_traces<<<n_traces, 256>>>(h->arrival.as<double>(), h->flow.as<int32_t>(), h->trace_off.as<int64_t>(),
+                                             h->trace_nf.as<int32_t>(), h->verr.as<unsigned long long>());
+        CK(cudaGetLastError());
+        unsigned long long e = 0;
+        CK(cudaMemcpy(&e, h->verr.p, 8, cudaMemcpyDeviceToHost));
+        if (e != ~0ull) {
+            const int t = (int)(e >> 29), kind = (int)(e & 3);
+            h->n_traces = 0; h->h_trace_off.assign(1, 0); h->h_trace_nf.clear(); h->prepared = false;
+            if (kind == 0) return set_err(GFQ_EINVAL, "gfq_upload_traces: flow id out of range in trace " + std::to_string(t));
+            if (kind == 1) return set_err(GFQ_EINVAL, "trace arrival times must be non-decreasing (trace " + std::to_string(t) + ")");
+            return set_err(GFQ_EINVAL, "gfq_upload_traces: arrival times must be finite and >= 0");
+        }
+    }
     return index_traces(h, off, n_flows, n_traces, foff_off, max_nf);
 }
 

@@ -133,3 +133,31 @@ def test_fast_and_generic_builds_agree_on_stats():
     assert np.array_equal(a[1], gen.get(_abi.OUT_FLOW_MEAN))
     assert np.array_equal(a[2], gen.counters[:, :4])
     eng.close()
+
+
+def test_trace_upload_validation_on_gpu():
+    """gfq_upload_traces validates every arrival on the GPU and reports the
+    first failure in (trace, position, check) order, as a sequential scan
+    would (engine.py:50-52,72-73); a failed upload leaves no traces resident."""
+    from paper_2507_08954_b200.engine import Engine
+    eng = Engine(0)
+    good = np.array([0.5, 1.0, 1.0, 2.0])
+    bad_t = np.array([0.5, 1.0, 0.9, 2.0])
+    off = np.array([0, 4, 8, 12], dtype=np.int64)
+    nf = np.array([2, 2, 2], dtype=np.int32)
+    fl = np.zeros(12, dtype=np.int32)
+
+    def up(arr, flow):
+        eng.upload_trace_arrays(np.ascontiguousarray(arr, dtype=np.float64),
+                                np.ascontiguousarray(flow, dtype=np.int32), off, nf)
+
+    with pytest.raises(ValueError, match=r"non-decreasing \(trace 2\)"):
+        up(np.concatenate([good, good, bad_t]), fl)
+    f2 = fl.copy(); f2[9] = 2; f2[6] = 5                  # trace 1 fails first
+    with pytest.raises(ValueError, match="flow id out of range in trace 1"):
+        up(np.concatenate([good, good, bad_t]), f2)
+    a3 = np.concatenate([good, good, good]); a3[5] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        up(a3, fl)
+    up(np.concatenate([good, good, good]), fl)            # a valid upload still works
+    eng.close()
