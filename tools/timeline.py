@@ -53,3 +53,10 @@ heap = [0.0] * slots
 for d_ in sorted(dur.tolist(), reverse=True):
     heapq.heapreplace(heap, heap[0] + d_)
 print(f"slots {slots}: perfect-knowledge LPT makespan {max(heap):.2f} ms vs measured {end:.2f} ms")
+
+out = os.environ.get("TIMELINE_OUT")
+if out:
+    np.savez(out, t0=t0, t1=t1, sm=sm, ev=ev,
+             T=np.array([s.t_overrun for s in w.sims]), alpha=np.array([s.alpha for s in w.sims]),
+             dcfg=np.array([s.device_cfg for s in w.sims]), trace=np.array([s.trace for s in w.sims]),
+             n=np.array([w.traces[s.trace].n for s in w.sims]), order_cost=np.zeros(len(w.sims)))
