@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ P
 // memory (or the flow/event part in a per-CTA global slice, FG).  Warp 0 runs
 // the event loop; warps 1.. serve its flow scans and event-pool argmins
 // (WarpSim::cta_scan / helper_loop, named barriers 1 and 2).
-template <bool FG>
+template <int POL, bool ND1, bool FG>
 __global__ void __launch_bounds__(GFQ_CTA_THREADS, 1) k_sim_cta(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_idx;
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(GFQ_CTA_THREADS, 1) k_sim_cta(const __grid_con
         __syncthreads();
         if (idx >= p.n_sims) break;
         const int sid = p.order[idx];
-        WarpSim<PB_GENERIC, false, true> w(p, base, fe, lane, sid);
+        WarpSim<POL, ND1, true> w(p, base, fe, lane, sid);
         w.wid = warp; w.nthr = blockDim.x; w.use_inf_ = 0;
         sim_setup(w, p, sid);
         sim_reset_flows(w, p, threadIdx.x, blockDim.x);
@@ -527,10 +527,17 @@ __global__ void k_trace_index(const int32_t* flow, const int64_t* trace_off, con
 using namespace gfq;
 
 // the k_sim instantiation of each kernel class (see gfq_prepare)
-enum { NCLASS = 7, CLASS_CTA = 6 };
+// CTA-mode classes: 6 generic, 7 MQFQ-Sticky and 8 FCFS on a 1-device DeviceSet
+enum { NCLASS = 9, CLASS_CTA = 6, CLASS_CTA_MQFQ1 = 7, CLASS_CTA_FCFS1 = 8 };
+static inline bool is_cta_class(int k) { return k >= CLASS_CTA; }
 static const void* class_kernel(int k, bool flows_global) {
     switch (k) {
-        case CLASS_CTA: return flows_global ? (const void*)k_sim_cta<true> : (const void*)k_sim_cta<false>;
+        case CLASS_CTA: return flows_global ? (const void*)k_sim_cta<PB_GENERIC, false, true>
+                                            : (const void*)k_sim_cta<PB_GENERIC, false, false>;
+        case CLASS_CTA_MQFQ1: return flows_global ? (const void*)k_sim_cta<PB_MQFQ, true, true>
+                                                  : (const void*)k_sim_cta<PB_MQFQ, true, false>;
+        case CLASS_CTA_FCFS1: return flows_global ? (const void*)k_sim_cta<PB_FCFS, true, true>
+                                                  : (const void*)k_sim_cta<PB_FCFS, true, false>;
         case 1: return (const void*)k_sim<PB_MQFQ, false, false>;
         case 2: return (const void*)k_sim<PB_MQFQ, true, false>;
         case 3: return (const void*)k_sim<PB_FCFS, true, false>;
@@ -617,8 +624,8 @@ struct gfq_handle {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     // kernel classes run concurrently on side streams (fork/join on the
     // caller's stream), so one class's tail overlaps the next class's start
-    cudaStream_t side[8] = {};
-    cudaEvent_t fork = nullptr, join[8] = {};
+    cudaStream_t side[16] = {};
+    cudaEvent_t fork = nullptr, join[16] = {};
     std::vector<cudaEvent_t> ring;          // GFQ_TIMING_RING x 3 events
     int ring_next = 0, ring_count = 0;
     cudaStream_t last_stream = nullptr;
@@ -1090,6 +1097,10 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         int k = 0;
         if (L.cta) {
             k = CLASS_CTA;
+            if (!logs && s.device_model == GFQ_DEVMODEL_DEVICESET && s.n_devices == 1) {
+                if (s.policy == GFQ_POLICY_MQFQ) k = CLASS_CTA_MQFQ1;
+                else if (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) k = CLASS_CTA_FCFS1;
+            }
         } else if (!logs && !L.flows_global && s.device_model == GFQ_DEVMODEL_DEVICESET) {
             if (s.n_devices == 1) {
                 k = s.policy == GFQ_POLICY_MQFQ ? 2
@@ -1110,8 +1121,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     for (int k = 0; k < NCLASS; k++) {
         if (!ccount[k]) continue;
         const void* kfn = class_kernel(k, L.flows_global);
-        const int threads = k == CLASS_CTA ? cta_threads : wpb * 32;
-        const int per_cta = k == CLASS_CTA ? 1 : wpb;   // simulations in flight per CTA
+        const int threads = is_cta_class(k) ? cta_threads : wpb * 32;
+        const int per_cta = is_cta_class(k) ? 1 : wpb;   // simulations in flight per CTA
         CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // all of the unified L1/shared array to shared memory: occupancy is bounded
         // by per-warp simulation state; the kernel's global traffic is tiny
@@ -1157,7 +1168,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
                                 (int)(rwpb * RED_FLOW_BYTES * L.F)));
     size_t gscr = 0;
     if (L.flows_global)
-        for (int k = 0; k < NCLASS; k++) gscr = std::max(gscr, (size_t)cblocks[k] * (k == CLASS_CTA ? 1 : wpb) * L.fe_bytes);
+        for (int k = 0; k < NCLASS; k++) gscr = std::max(gscr, (size_t)cblocks[k] * (is_cta_class(k) ? 1 : wpb) * L.fe_bytes);
     if (rglobal) gscr = std::max(gscr, (size_t)rblocks * rwpb * RED_FLOW_BYTES * L.F);
     const int64_t rper = std::max(max_n, 1);              // reducer record scratch per warp
 
@@ -1336,7 +1347,7 @@ int gfq_launch(gfq_handle* h, void* stream) {
             pk.order = p.order + off;
             pk.n_sims = h->ccount[k];
             pk.work = p.work + k;
-            dim3 g(h->cblocks[k]), b(k == CLASS_CTA ? h->cta_threads : h->wpb * 32);
+            dim3 g(h->cblocks[k]), b(is_cta_class(k) ? h->cta_threads : h->wpb * 32);
             void* args[] = {&pk};
             cudaStream_t ks = st;
             if (fork) {

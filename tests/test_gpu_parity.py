@@ -139,6 +139,26 @@ def test_cta_build(engine, flags):
     assert not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
 
 
+@pytest.mark.parametrize("flags", ["cta", "cta+global"])
+def test_cta_fast_builds(engine, flags):
+    """The specialised CTA builds (MQFQ-Sticky / FCFS on a 1-device
+    DeviceSet, device state in registers), forced on every such golden case
+    with every scan on the CTA path: dispatch rows, records and statistics
+    must match the reference."""
+    from gpu_harness import compare_to_golden, run_cases
+    from paper_2507_08954_b200 import _abi
+    cases = [c for c in all_cases() if not c.get("scripted")
+             and c.get("policy", "mqfq") in ("mqfq", "fcfs", "fcfs_naive")
+             and len(c.get("devices", [{}])) == 1]
+    f = _abi.FLAG_CTA | (_abi.FLAG_FLOWS_GLOBAL if "global" in flags else 0)
+    outs, _ = run_cases(cases, engine, early_exit=True, flags=f,
+                        outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH)
+    gold = golden()
+    bad = {c["name"]: m for c, o in zip(cases, outs)
+           if (m := compare_to_golden(o, gold[c["name"]], exact_keys=("dispatch", "records")))}
+    assert cases and not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
+
+
 def test_c4_large_flow_sims_match_oracle(engine):
     """BASELINE C4: 4096 functions per simulation (2.1k touched), pool 32/256,
     heterogeneous memory, MQFQ + FCFS: flows-in-global build vs the oracle."""
