@@ -876,10 +876,10 @@ struct WarpSim {
     FI int monitor_tick(int d, double util, int id) {
         const int S = P.L.S;
         int head = DV(d, DV_SHEAD), ns = DV(d, DV_SN);
-        // S = ceil(window / period) + 3 > the samples a window can hold; the
-        // check only guards against a mis-sized ring (the run is failed and
-        // its outputs discarded, so clamping keeps the hot path branch-free)
-        if (UNLIKELY(ns >= S)) { fail(GFQ_SIM_SAMPLE_OVERFLOW); ns = S - 1; }
+        // No overflow check: samples are a tick period apart and a window
+        // keeps those newer than now - window, so at most
+        // ceil(window / period) + 2 are held here, and gfq_prepare sizes
+        // S = ceil(window / period) + 3 (the min period over the devices).
         int w = head + ns; if (w >= S) w -= S;
         const uint32_t code = ((uint32_t)DV(d, DV_WCODE) << 4) | (uint32_t)id;
         const int zage = id ? min(DV(d, DV_ZAGE) + 1, 15) : 0;
