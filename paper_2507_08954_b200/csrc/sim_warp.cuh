@@ -902,31 +902,36 @@ struct WarpSim {
             key = (code & ((1u << (4 * ns)) - 1u)) | ((uint32_t)ns << 28);
             slot = (int)((key * 0x9E3779B1u) >> (32 - WMEMO_BITS));
         }
-        if (memo && key == (uint32_t)DV(d, DV_LKEY)) {  // same window as the last tick
-            avg = UAVG(d);
-        } else if (LIKELY(memo && WKEY(d, slot) == key)) {
-            avg = WVAL(d, slot);
-            diag(DG_WHIT);
-        } else {
-            diag(DG_WMISS);
-            PySum a; ps_init(a);
-            int j = head;
-            #pragma unroll 1
-            for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
-            avg = ps_val(a) / (double)ns;
-            if (memo) { USYNC(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
-        }
         int effd = DV(d, DV_EFFD), hrok = DV(d, DV_HROK);
-        const bool dyn = DV(d, DV_DYN);
-        // a fixed D and an unchanged average leave effective_d and the
-        // headroom check as they were
-        if (dyn || __double_as_longlong(avg) != __double_as_longlong(UAVG(d))) {
-            const int dmax = DV(d, DV_DMAX);
-            const double thr = DD(d, DD_THR), inv = DD(d, DD_INVDMAX);
-            if (!dyn) effd = dmax;
-            else if (avg > thr) effd = max(effd - 1, 1);
-            else if (avg < thr - inv) effd = min(effd + 1, dmax);
-            hrok = !(avg + inv > thr);                                  // device.py:137-139
+        if (memo && key == (uint32_t)DV(d, DV_LKEY)) {
+            // same window as the last tick: the same average, and (the key is
+            // only kept for a fixed D) the same effective_d and headroom flag
+            avg = UAVG(d);
+        } else {
+            if (LIKELY(memo && WKEY(d, slot) == key)) {
+                avg = WVAL(d, slot);
+                diag(DG_WHIT);
+            } else {
+                diag(DG_WMISS);
+                PySum a; ps_init(a);
+                int j = head;
+                #pragma unroll 1
+                for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
+                avg = ps_val(a) / (double)ns;
+                if (memo) { USYNC(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
+            }
+            const bool dyn = DV(d, DV_DYN);
+            // a fixed D and an unchanged average leave effective_d and the
+            // headroom check as they were
+            if (dyn || __double_as_longlong(avg) != __double_as_longlong(UAVG(d))) {
+                const int dmax = DV(d, DV_DMAX);
+                const double thr = DD(d, DD_THR), inv = DD(d, DD_INVDMAX);
+                if (!dyn) effd = dmax;
+                else if (avg > thr) effd = max(effd - 1, 1);
+                else if (avg < thr - inv) effd = min(effd + 1, dmax);
+                hrok = !(avg + inv > thr);                              // device.py:137-139
+            }
+            if (dyn) key = 0xffffffffu;                  // dynamic D moves every tick
         }
         if (!ND1) __syncwarp();                          // 1-device build: registers
         DV(d, DV_SHEAD) = head; DV(d, DV_SN) = ns; UAVG(d) = avg; DV(d, DV_EFFD) = effd;
