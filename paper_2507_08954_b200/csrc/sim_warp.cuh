@@ -1490,13 +1490,21 @@ struct WarpSim {
                 // a pooled event was pushed before the tick): the run ends at
                 // the first tick with time >= lim.
                 const double lim = pymin(t_arr, pmin_slot >= 0 ? pmin_t : INF);
+                // quiet_drain() with the terms a run cannot change hoisted: no
+                // dispatch, completion or refresh happens inside it, so only
+                // the clock (keep-alive bound) and the device window's
+                // effective_d / headroom flag move from tick to tick
+                const bool q_gvt = !MQFQ || gmin_ok;
+                const bool q_idle = tot_pend == 0, q_busy = tot_infl > 0;
                 #pragma unroll 1
                 for (;;) {
                     tick_on = false;
                     diag(DG_TICKS);
                     log_event(now, EV_TICK, -1);
                     on_monitor();
-                    if (UNLIKELY(status) || !quiet_drain()) break;
+                    const bool quiet = q_gvt && (!MQFQ || now < idle_lb) &&
+                                       (q_idle || (q_busy && certain_refusal()));
+                    if (UNLIKELY(status) || !quiet) break;
                     n_calls++;
                     diag(DG_QUIET);
                     dr = false;
