@@ -332,8 +332,9 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
     w.now = 0.0; w.gvt = 0.0;
     w.seq = (uint32_t)w.n;
     w.cursor = 0; w.nev = 0;
-    w.tick_on = false; w.tick_t = 0.0; w.tick_seq = 0;
-    w.pmin_ok = true; w.pmin_t = 0.0; w.pmin_seq = 0; w.pmin_slot = -1;
+    // an absent tick / pooled event keeps its time at +inf (event selection)
+    w.tick_on = false; w.tick_t = __longlong_as_double(0x7ff0000000000000ll); w.tick_seq = 0;
+    w.pmin_ok = true; w.pmin_t = __longlong_as_double(0x7ff0000000000000ll); w.pmin_seq = 0; w.pmin_slot = -1;
     w.tot_pend = 0; w.tot_infl = 0;
     w.fcfs_head = 0; w.fcfs_infl = 0; w.draining = -1;
     w.s_att = 0; w.s_out = 0; w.s_exec = 0;

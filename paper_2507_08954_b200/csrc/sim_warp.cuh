@@ -514,7 +514,7 @@ struct WarpSim {
         if (cta_on(nev)) {
             Arg a = cta_scan(OP_EVMIN);
             pmin_ok = true;
-            if (a.i == 0x7fffffff) { pmin_slot = -1; return; }
+            if (a.i == 0x7fffffff) { pmin_slot = -1; pmin_t = __longlong_as_double(0x7ff0000000000000ll); return; }
             pmin_slot = a.i; pmin_t = from_key(a.k); pmin_seq = a.s;
             return;
         }
@@ -528,7 +528,7 @@ struct WarpSim {
         uint32_t ms = wmin32(bt == m ? bs : 0xffffffffu);
         int src = __ffs(__ballot_sync(FULLMASK, bt == m && bs == ms && bslot >= 0)) - 1;
         pmin_ok = true;
-        if (src < 0) { pmin_slot = -1; return; }
+        if (src < 0) { pmin_slot = -1; pmin_t = __longlong_as_double(0x7ff0000000000000ll); return; }
         pmin_slot = __shfl_sync(FULLMASK, bslot, src);
         pmin_t = from_key(m); pmin_seq = ms;
     }
@@ -1402,7 +1402,7 @@ struct WarpSim {
             if (G) __syncwarp();
         }
         if (cursor < n || tot_pend > 0 || tot_infl > 0) push_tick(now + period);
-        else tick_on = false;
+        else { tick_on = false; tick_t = __longlong_as_double(0x7ff0000000000000ll); }
     }
 
     FI void on_expiry(int fn) {                           // engine.py:167-171
@@ -1458,12 +1458,13 @@ struct WarpSim {
                 if (early && cursor >= n && tot_pend == 0 && tot_infl == 0) break;
             }
             // earliest (time, seq): arrivals (seq = trace index < every dynamic
-            // seq) win time ties; absent candidates sit at +inf
-            const double tt = tick_on ? tick_t : INF, tp = pmin_slot >= 0 ? pmin_t : INF;
+            // seq) win time ties.  An absent tick or pooled event keeps its time
+            // at +inf (tick_t / pmin_t invariants), and with neither present and
+            // no arrival left the loop has ended above, so no +inf tie remains.
             int kind; double t;
-            if (t_arr <= tt && t_arr <= tp && t_arr != INF) { kind = EV_ARRIVAL; t = t_arr; }
-            else if (tick_on && (tt < tp || (tt == tp && tick_seq < pmin_seq))) { kind = EV_TICK; t = tt; }
-            else { kind = 4; t = tp; }
+            if (t_arr <= tick_t && t_arr <= pmin_t && t_arr != INF) { kind = EV_ARRIVAL; t = t_arr; }
+            else if (tick_t < pmin_t || (tick_t == pmin_t && tick_seq < pmin_seq)) { kind = EV_TICK; t = tick_t; }
+            else { kind = 4; t = pmin_t; }
             if (UNLIKELY(n_events >= max_events)) { fail(GFQ_SIM_WATCHDOG); break; }
             now = t;
             n_events++;
@@ -1489,7 +1490,7 @@ struct WarpSim {
                 // time tie with the tick (an arrival's seq is its trace index;
                 // a pooled event was pushed before the tick): the run ends at
                 // the first tick with time >= lim.
-                const double lim = pymin(t_arr, pmin_slot >= 0 ? pmin_t : INF);
+                const double lim = pymin(t_arr, pmin_t);
                 // quiet_drain() with the terms a run cannot change hoisted: no
                 // dispatch, completion or refresh happens inside it, so only
                 // the clock (keep-alive bound) and the device window's
