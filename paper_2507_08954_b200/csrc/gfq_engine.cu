@@ -393,9 +393,12 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
 #ifndef GFQ_MINB
 #define GFQ_MINB 4
 #endif
+#ifndef GFQ_KTHREADS                      // k_sim block size bound (simulations per CTA x 32)
+#define GFQ_KTHREADS 128
+#endif
 
 template <int POL, bool ND1, bool FG>
-__global__ void __launch_bounds__(128, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(GFQ_KTHREADS, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* slice = smem + (size_t)warp * p.L.bytes;
@@ -1114,7 +1117,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
         cls[i] = k;
         ccount[k]++;
     }
-    int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, 4) : 4;
+    int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, GFQ_KTHREADS / 32) : GFQ_KTHREADS / 32;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
     if (L.cta) wpb = 1;                       // one simulation (workspace) per CTA
     size_t smem = (size_t)wpb * L.bytes;

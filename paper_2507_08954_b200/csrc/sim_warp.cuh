@@ -125,9 +125,12 @@ FI double pymin(double a, double b) { return b < a ? b : a; }
 struct PySum { double f, c; };
 FI void ps_init(PySum& s) { s.f = 0.0; s.c = 0.0; }
 FI void ps_add(PySum& s, double x) {
-    double t = s.f + x;
-    double e1 = (s.f - t) + x, e2 = (x - t) + s.f;
-    s.c += fabs(s.f) >= fabs(x) ? e1 : e2;
+    // c += (f - t) + x if |f| >= |x| else (x - t) + f: the operands are
+    // selected first, so one compensation term is computed, not two
+    const double t = s.f + x;
+    const bool big = fabs(s.f) >= fabs(x);
+    const double a = big ? s.f : x, b = big ? x : s.f;
+    s.c += (a - t) + b;
     s.f = t;
 }
 FI double ps_val(const PySum& s) {
