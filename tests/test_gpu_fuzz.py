@@ -1,11 +1,13 @@
 """Randomised parity: 480 random simulations (every policy; 1-3 devices;
 D, T, alpha, default TTL, pool size / disabled, dynamic D, utilisation
 threshold and window, PCIe bandwidth, prefetch overlap, interference,
-heterogeneous profiles) run as one batch through the fast kernel classes
-(statistics + records + dispatch rows, early exit) and checked against the
-C oracle: dispatch rows and completion records bit for bit, per-function
-statistics and the run summary within 1e-9.  Complements the 1560 golden
-cases with configurations nobody hand-picked."""
+heterogeneous profiles) run as one batch and checked against the C oracle:
+dispatch rows and completion records bit for bit, per-function statistics
+and the run summary within 1e-9.  The batch runs through each build: the
+specialised warp classes (statistics + records + dispatch rows, early
+exit), the generic class (audit logs requested), flows in global memory, and
+CTA-per-simulation.  Complements the 1560 golden cases with configurations
+nobody hand-picked."""
 
 from __future__ import annotations
 
@@ -66,17 +68,25 @@ def _workload(rng, n_sims):
     return traces, tabs, dcfgs, sims, _abi
 
 
-def test_random_configs_match_oracle():
+BUILDS = {"fast": (0, 0), "generic": (0, 1), "flows_global": (1, 0), "cta": (2, 0)}
+
+
+@pytest.mark.parametrize("build", list(BUILDS))
+def test_random_configs_match_oracle(build):
     from oracle import oracle as orc
     from paper_2507_08954_b200.engine import BatchResult, Engine
     rng = np.random.default_rng(20261017)
-    traces, tabs, dcfgs, sims, _abi = _workload(rng, 480)
+    traces, tabs, dcfgs, sims, _abi = _workload(rng, 480 if build == "fast" else 160)
+    flags, audit = BUILDS[build]
     eng = Engine(0)
     eng.upload_traces(traces)
     eng.upload_flowtabs(tabs)
     eng.upload_device_cfgs(dcfgs)
-    eng.run(sims, outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH,
-            early_exit=True)
+    outputs = _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH
+    if audit:
+        outputs |= _abi.WANT_AUDIT
+    kw = {"audit_util_cap": 1 << 17} if audit else {}          # overloaded sims tick long
+    eng.run(sims, outputs=outputs, early_exit=True, flags=flags, **kw)
     res = BatchResult(eng)
     bad = []
     for i, s in enumerate(sims):
