@@ -144,6 +144,9 @@ typedef struct gfq_launch_cfg {
                                       flow count does not fit shared memory)           */
 #define GFQ_FLAG_CTA          0x2u /* one simulation per CTA, every scan split over its
                                       warps (automatic for large flow counts)          */
+#define GFQ_FLAG_WARP         0x4u /* never CTA-per-simulation: one simulation per warp,
+                                      per-flow state in global scratch when it does not
+                                      fit (many large-flow simulations at once)        */
 
 #define GFQ_NCOUNTERS 12
 

@@ -18,6 +18,7 @@ MAX_DEVICES = 8
 NCOUNTERS = 12
 FLAG_FLOWS_GLOBAL = 0x1
 FLAG_CTA = 0x2
+FLAG_WARP = 0x4
 
 SIM_STATUS = {
     0: "ok",

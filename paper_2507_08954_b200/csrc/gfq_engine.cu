@@ -1061,11 +1061,27 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     // shared memory, or GFQ_FLAG_CTA): one simulation per CTA, its scans split
     // over the CTA's warps.  The CTA gets 512 threads (256 when two such
     // simulations fit an SM).
+    //
+    // Unless the batch is large: then the warp build with the flow state in
+    // global scratch (16 simulations per SM instead of 1-2) finishes first.
+    // Measured on BASELINE C4 (4096 functions, ~2.1k touched): a warp
+    // simulation takes ~6x as long as a CTA one, so the warp build wins once
+    // the CTA build would need more than 6 waves per warp-build wave
+    // (2368 simulations: 23M vs 9M dispatches/s).  GFQ_FLAG_CTA / GFQ_FLAG_WARP
+    // force either.
     int cta_threads = 0;
-    if ((c.flags & GFQ_FLAG_CTA) || (size_t)4 * L.bytes > h->smem_optin) {
-        L.cta = 1;
-        layout_finish(L);
-        cta_threads = (size_t)2 * L.bytes <= h->smem_optin ? 256 : GFQ_CTA_THREADS;
+    const bool big = (size_t)4 * L.bytes > h->smem_optin;    // warp build: flows in global scratch
+    if (!(c.flags & GFQ_FLAG_WARP) && ((c.flags & GFQ_FLAG_CTA) || big)) {
+        Layout Lc = L;
+        Lc.cta = 1;
+        layout_finish(Lc);
+        const int cta_per_sm = (size_t)2 * Lc.bytes <= h->smem_optin ? 2 : 1;
+        const long long cta_waves = (n_sims + (long long)cta_per_sm * h->n_sm - 1) / ((long long)cta_per_sm * h->n_sm);
+        const long long warp_waves = (n_sims + 16ll * h->n_sm - 1) / (16ll * h->n_sm);
+        if ((c.flags & GFQ_FLAG_CTA) || cta_waves <= 6 * warp_waves) {
+            L = Lc;
+            cta_threads = cta_per_sm == 2 ? 256 : GFQ_CTA_THREADS;
+        }
     }
     // flow counts whose per-simulation state does not fit in shared memory
     // (or GFQ_FLAG_FLOWS_GLOBAL) put the flow/event part in global scratch
@@ -1082,7 +1098,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
             layout_finish(L);
         }
     }
-    if ((c.flags & GFQ_FLAG_FLOWS_GLOBAL) || (size_t)L.bytes > smem_avail) {
+    if ((c.flags & GFQ_FLAG_FLOWS_GLOBAL) || (size_t)L.bytes > smem_avail || (big && !L.cta)) {
         L.flows_global = 1;
         layout_finish(L);
     }

@@ -14,12 +14,13 @@ from paper_2507_08954_b200 import _abi, sweep
 from paper_2507_08954_b200.engine import Engine
 
 
-def check(n_seeds: int = 1, eng: Engine | None = None) -> list[str]:
+def check(n_seeds: int = 1, eng: Engine | None = None, flags: int = 0) -> list[str]:
     w = sweep.c4(n_seeds=n_seeds)
     own = eng is None
     eng = eng or Engine(0)
     w.upload(eng)
-    res = eng.run(w.sims_array(), outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH)
+    res = eng.run(w.sims_array(), outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH,
+                  flags=flags)
     bad = []
     for i, s in enumerate(w.sims):
         tr, tab = w.traces[s.trace], w.tabs[s.flowtab]

@@ -159,8 +159,34 @@ def test_cta_fast_builds(engine, flags):
     assert cases and not bad, f"{len(bad)}/{len(cases)} differ: {dict(list(bad.items())[:6])}"
 
 
-def test_c4_large_flow_sims_match_oracle(engine):
+@pytest.mark.parametrize("build", ["auto", "warp"])
+def test_c4_large_flow_sims_match_oracle(engine, build):
     """BASELINE C4: 4096 functions per simulation (2.1k touched), pool 32/256,
-    heterogeneous memory, MQFQ + FCFS: flows-in-global build vs the oracle."""
+    heterogeneous memory, MQFQ + FCFS vs the oracle: the CTA-per-simulation
+    build a small batch gets, and the warp build with the flow state in global
+    scratch that a large batch gets (GFQ_FLAG_WARP)."""
     from c4_check import check
-    assert check(1, engine) == []
+    from paper_2507_08954_b200 import _abi
+    assert check(1, engine, _abi.FLAG_WARP if build == "warp" else 0) == []
+
+
+def test_large_flow_batch_build_choice(engine):
+    """Large-flow simulations: a batch of one wave per SM runs CTA-per-simulation;
+    a batch that would need more than 6 CTA waves per warp-build wave runs the
+    warp build with the flow state in global scratch (gfq_prepare's rule)."""
+    import torch
+    from paper_2507_08954_b200 import _abi, sweep
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    w = sweep.c4(n_seeds=1)
+    w.upload(engine)
+    s0 = w.sims[0]
+    small = (_abi.Sim * n_sm)(*([s0] * n_sm))
+    engine.prepare(small, outputs=_abi.WANT_STATS)
+    info = engine.batch_info()
+    assert info["cta_threads"] > 0 and not info["flows_global"], info
+    big = (_abi.Sim * (16 * n_sm))(*([s0] * (16 * n_sm)))
+    engine.prepare(big, outputs=_abi.WANT_STATS)
+    info = engine.batch_info()
+    assert info["cta_threads"] == 0 and info["flows_global"], info
+    engine.prepare(big, outputs=_abi.WANT_STATS, flags=_abi.FLAG_CTA)
+    assert engine.batch_info()["cta_threads"] > 0
