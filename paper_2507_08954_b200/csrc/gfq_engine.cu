@@ -237,8 +237,8 @@ __device__ __forceinline__ void reduce_one(const Params& p, unsigned char* base,
 
 
 // Per-simulation member setup (every thread that touches the simulation).
-template <int POL, bool ND1, bool CTA>
-__device__ __forceinline__ void sim_setup(WarpSim<POL, ND1, CTA>& w, const Params& p, int sid) {
+template <int POL, bool ND1, bool CTA, bool FG>
+__device__ __forceinline__ void sim_setup(WarpSim<POL, ND1, CTA, FG>& w, const Params& p, int sid) {
     constexpr bool G = POL == PB_GENERIC;
     const gfq_sim* sim = p.sims + sid;
     w.sim = sim;
@@ -260,8 +260,8 @@ __device__ __forceinline__ void sim_setup(WarpSim<POL, ND1, CTA>& w, const Param
 }
 
 // Zero the per-flow state and container counts (threads t, t+st, ...).
-template <int POL, bool ND1, bool CTA>
-__device__ __forceinline__ void sim_reset_flows(WarpSim<POL, ND1, CTA>& w, const Params& p, int t, int st) {
+template <int POL, bool ND1, bool CTA, bool FG>
+__device__ __forceinline__ void sim_reset_flows(WarpSim<POL, ND1, CTA, FG>& w, const Params& p, int t, int st) {
     double *vt = w.vt(), *lex = w.lex(), *tau = w.tau(), *iat = w.iat(), *larr = w.larr();
     int *pt = w.pt(), *ph = w.ph(), *infl = w.infl(), *head = w.head(), *done = w.done(), *pend = w.pend();
     uint8_t* fst = w.fst();
@@ -274,8 +274,8 @@ __device__ __forceinline__ void sim_reset_flows(WarpSim<POL, ND1, CTA>& w, const
 }
 
 // Device state reset, the event loop and the per-simulation outputs (one warp).
-template <int POL, bool ND1, bool CTA>
-__device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params& p, int sid) {
+template <int POL, bool ND1, bool CTA, bool FG>
+__device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA, FG>& w, const Params& p, int sid) {
     constexpr bool G = POL == PB_GENERIC;
     const gfq_sim* sim = w.sim;
     const int lane = w.lane;
@@ -380,10 +380,10 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA>& w, const Params&
     __syncwarp();
 }
 
-template <int POL, bool ND1>
+template <int POL, bool ND1, bool FG>
 __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, unsigned char* fe,
                                         int lane, int sid) {
-    WarpSim<POL, ND1> w(p, base, fe, lane, sid);
+    WarpSim<POL, ND1, false, FG> w(p, base, fe, lane, sid);
     sim_setup(w, p, sid);
     sim_reset_flows(w, p, lane, 32);
     __syncwarp();
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(GFQ_KTHREADS, GFQ_MINB) k_sim(const __grid_con
         if (lane == 0) idx = atomicAdd(p.work, 1);
         idx = __shfl_sync(FULLMASK, idx, 0);
         if (idx >= p.n_sims) break;
-        run_one<POL, ND1>(p, base, fe, lane, p.order[idx]);
+        run_one<POL, ND1, FG>(p, base, fe, lane, p.order[idx]);
     }
 }
 
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(GFQ_CTA_THREADS, 1) k_sim_cta(const __grid_con
         __syncthreads();
         if (idx >= p.n_sims) break;
         const int sid = p.order[idx];
-        WarpSim<POL, ND1, true> w(p, base, fe, lane, sid);
+        WarpSim<POL, ND1, true, FG> w(p, base, fe, lane, sid);
         w.wid = warp; w.nthr = blockDim.x; w.use_inf_ = 0;
         sim_setup(w, p, sid);
         sim_reset_flows(w, p, threadIdx.x, blockDim.x);
@@ -543,8 +543,10 @@ static const void* class_kernel(int k, bool flows_global) {
         case CLASS_CTA_FCFS1: return flows_global ? (const void*)k_sim_cta<PB_FCFS, true, true>
                                                   : (const void*)k_sim_cta<PB_FCFS, true, false>;
         case 1: return (const void*)k_sim<PB_MQFQ, false, false>;
-        case 2: return (const void*)k_sim<PB_MQFQ, true, false>;
-        case 3: return (const void*)k_sim<PB_FCFS, true, false>;
+        case 2: return flows_global ? (const void*)k_sim<PB_MQFQ, true, true>
+                                    : (const void*)k_sim<PB_MQFQ, true, false>;
+        case 3: return flows_global ? (const void*)k_sim<PB_FCFS, true, true>
+                                    : (const void*)k_sim<PB_FCFS, true, false>;
         case 4: return (const void*)k_sim<PB_BATCH, true, false>;
         case 5: return (const void*)k_sim<PB_SJF, true, false>;
         default: return flows_global ? (const void*)k_sim<PB_GENERIC, false, true>
@@ -1109,6 +1111,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     //   0 generic (any policy, scripted devices, audit / event logs, large F)
     //   1 MQFQ-Sticky on a multi-device DeviceSet
     //   2..5 one policy (MQFQ / FCFS / Batch / SJF) on a 1-device DeviceSet
+    //        (flows in global scratch: MQFQ / FCFS only)
     const bool logs = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
     std::vector<int> cls(n_sims);
     int ccount[NCLASS] = {0};
@@ -1121,12 +1124,13 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
                 if (s.policy == GFQ_POLICY_MQFQ) k = CLASS_CTA_MQFQ1;
                 else if (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) k = CLASS_CTA_FCFS1;
             }
-        } else if (!logs && !L.flows_global && s.device_model == GFQ_DEVMODEL_DEVICESET) {
+        } else if (!logs && s.device_model == GFQ_DEVMODEL_DEVICESET) {
             if (s.n_devices == 1) {
                 k = s.policy == GFQ_POLICY_MQFQ ? 2
                   : (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) ? 3
                   : s.policy == GFQ_POLICY_BATCH ? 4 : 5;
-            } else if (s.policy == GFQ_POLICY_MQFQ) {
+                if (L.flows_global && k > 3) k = 0;       // flows in global: MQFQ / FCFS builds only
+            } else if (s.policy == GFQ_POLICY_MQFQ && !L.flows_global) {
                 k = 1;
             }
         }

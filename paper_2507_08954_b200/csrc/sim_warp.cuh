@@ -197,9 +197,13 @@ FI void cta_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(
 // CTA = one simulation per CTA (large flow counts): warp 0
 // (the leader) runs everything below; the O(F) flow scans and the event-pool
 // argmin are split over all the CTA's warps (cta_scan / helper_loop).
-template <int POL, bool ND1, bool CTA = false>
+template <int POL, bool ND1, bool CTA = false, bool FG = false>
 struct WarpSim {
     static constexpr bool G = POL == PB_GENERIC;
+    // FG: the flow/event part lives in global scratch; its lane-strided scans
+    // keep several loads in flight (a smem build keeps them rolled: its hot
+    // code size is what bounds it)
+    static constexpr int SCAN_UNROLL = FG ? 4 : 1;
     static constexpr bool RING = CTA && GFQ_RING;
     static constexpr bool CSTAGE = CTA && GFQ_CSTAGE;
     const Params& P;
@@ -522,7 +526,7 @@ struct WarpSim {
             return;
         }
         u64 bt = ~0ull; uint32_t bs = 0xffffffffu; int bslot = -1;
-        #pragma unroll 1
+        #pragma unroll SCAN_UNROLL
         for (int i = lane; i < nev; i += 32) {
             u64 k = okey(ev_t()[i]); uint32_t s = ev_seq()[i];
             if (k < bt || (k == bt && s < bs)) { bt = k; bs = s; bslot = i; }
@@ -958,7 +962,7 @@ struct WarpSim {
         if (UNLIKELY(!gmin_ok)) {
             diag(DG_GSCAN);
             u64 bk = ~0ull;
-            #pragma unroll 1
+            #pragma unroll SCAN_UNROLL
             for (int f = lane; f < nf; f += 32)
                 if (pt()[f] - done()[f] > 0) { u64 k = okey(vt()[f]); if (k < bk) bk = k; }
             gmin = wmin64(bk);
@@ -1038,7 +1042,7 @@ struct WarpSim {
             return m == ~0ull ? -1 : (int)(m & 0xffffu);
         }
         u64 bk = ~0ull;
-        #pragma unroll 1
+        #pragma unroll SCAN_UNROLL
         for (int f = lane; f < nf; f += 32) {
             int pe = pend()[f];
             if (pe > 0 && vt()[f] - gvt <= T) {
@@ -1063,7 +1067,7 @@ struct WarpSim {
             return m == ~0ull ? -1 : flw((int)m);
         }
         unsigned bk = 0xffffffffu;
-        #pragma unroll 1
+        #pragma unroll SCAN_UNROLL
         for (int f = lane; f < nf; f += 32)
             if (pend()[f] > 0) bk = min(bk, (unsigned)head()[f]);
         unsigned m = wmin32(bk);
@@ -1078,7 +1082,7 @@ struct WarpSim {
             return a.k == ~0ull ? -1 : a.i;
         }
         u64 bk = ~0ull; int bf = 0x7fffffff;
-        #pragma unroll 1
+        #pragma unroll SCAN_UNROLL
         for (int f = lane; f < nf; f += 32)
             if (pend()[f] > 0) { u64 k = okey(tau()[f]); if (k < bk) { bk = k; bf = f; } }
         u64 m = wmin64(bk);
@@ -1245,7 +1249,7 @@ struct WarpSim {
                 ust(fst()[f], (uint8_t)((fst()[f] & ~FL_NEWLY) | FL_MARKED));
             }
         } else {                             // list overflow: scan every flow
-            #pragma unroll 1
+            #pragma unroll SCAN_UNROLL
             for (int f = lane; f < nf; f += 32) {
                 uint8_t s = fst()[f];
                 if (s & FL_NEWLY) {
