@@ -197,13 +197,16 @@ FI void cta_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(
 // CTA = one simulation per CTA (large flow counts): warp 0
 // (the leader) runs everything below; the O(F) flow scans and the event-pool
 // argmin are split over all the CTA's warps (cta_scan / helper_loop).
+#ifndef GFQ_FG_UNROLL
+#define GFQ_FG_UNROLL 8
+#endif
 template <int POL, bool ND1, bool CTA = false, bool FG = false>
 struct WarpSim {
     static constexpr bool G = POL == PB_GENERIC;
     // FG: the flow/event part lives in global scratch; its lane-strided scans
     // keep several loads in flight (a smem build keeps them rolled: its hot
     // code size is what bounds it)
-    static constexpr int SCAN_UNROLL = FG ? 4 : 1;
+    static constexpr int SCAN_UNROLL = FG ? GFQ_FG_UNROLL : 1;
     static constexpr bool RING = CTA && GFQ_RING;
     static constexpr bool CSTAGE = CTA && GFQ_CSTAGE;
     const Params& P;
