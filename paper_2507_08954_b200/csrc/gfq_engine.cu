@@ -621,6 +621,7 @@ struct gfq_handle {
     int cta_threads = 0, cta_min = 64;
     bool rglobal = false;
     int ccount[NCLASS] = {0}, cblocks[NCLASS] = {0};   // per kernel class
+    Layout Lk[NCLASS] = {};                              // per-class workspace layout
     bool prepared = false;
     DBuf out[GFQ_OUT_COUNT_];
     int64_t out_n[GFQ_OUT_COUNT_] = {0};
@@ -1140,11 +1141,22 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     int wpb = c.warps_per_block > 0 ? std::min(c.warps_per_block, GFQ_KTHREADS / 32) : GFQ_KTHREADS / 32;
     while (wpb > 1 && (size_t)wpb * L.bytes > h->smem_optin) wpb--;
     if (L.cta) wpb = 1;                       // one simulation (workspace) per CTA
-    size_t smem = (size_t)wpb * L.bytes;
     int cblocks[NCLASS] = {0};
+    // Per-class layouts: FCFS / Batch / SJF on one device (classes 3-5) never
+    // pool keep-alive expiries, so their dynamic events are completions, one
+    // per token at most; their smaller workspace raises their occupancy
+    // (C2: 18.8 -> 13.9 KB per simulation, 12 -> 16 warps per SM).
+    Layout Lk[NCLASS];
+    for (int k = 0; k < NCLASS; k++) Lk[k] = L;
+    if (!L.cta && !L.flows_global && c.event_capacity <= 0) {
+        const int32_t e_tok = std::max(64, (2 * R * nd + 32 + 31) & ~31);
+        for (int k = 3; k <= 5; k++)
+            if (e_tok < L.E) { Lk[k].E = e_tok; layout_finish(Lk[k]); }
+    }
     for (int k = 0; k < NCLASS; k++) {
         if (!ccount[k]) continue;
         const void* kfn = class_kernel(k, L.flows_global);
+        const size_t smem = (size_t)(is_cta_class(k) ? 1 : wpb) * Lk[k].bytes;
         const int threads = is_cta_class(k) ? cta_threads : wpb * 32;
         const int per_cta = is_cta_class(k) ? 1 : wpb;   // simulations in flight per CTA
         CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1267,7 +1279,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->rblocks = rblocks;
     h->rglobal = rglobal;
     h->rscr_per_warp = rper;
-    for (int k = 0; k < NCLASS; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; }
+    for (int k = 0; k < NCLASS; k++) { h->ccount[k] = ccount[k]; h->cblocks[k] = cblocks[k]; h->Lk[k] = Lk[k]; }
     h->prepared = true;
     h->launched = false;
     return GFQ_OK;
@@ -1348,7 +1360,6 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaEventRecord(h->ev[0], st));
     CK(cudaEventRecord(re[0], st));
     if (h->n_sims > 0) {
-        size_t smem = (size_t)h->wpb * h->L.bytes;
         int active = 0;
         for (int k = 0; k < NCLASS; k++) active += h->ccount[k] > 0;
         // several classes: fork onto side streams (not with flows in global
@@ -1368,6 +1379,8 @@ int gfq_launch(gfq_handle* h, void* stream) {
         for (int k = 0; k < NCLASS; k++) {
             if (!h->ccount[k]) continue;
             Params pk = p;
+            pk.L = h->Lk[k];
+            const size_t smem = (size_t)h->wpb * pk.L.bytes;
             pk.order = p.order + off;
             pk.n_sims = h->ccount[k];
             pk.work = p.work + k;
