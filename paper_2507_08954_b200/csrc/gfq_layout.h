@@ -41,7 +41,9 @@ enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };
 // CTA mode: the leader warp's scan command and the per-warp partial argmins
 // (lexicographic (k, s, i)) the helper warps return.
 enum { CTA_MAXW = 32 };
+#ifndef GFQ_CTA_THREADS
 #define GFQ_CTA_THREADS 512        // threads of a CTA-mode simulation (max)
+#endif
 struct CtaCmd {
     int32_t op, nf, nev, iarg;     // scan kind, flow count, event slots, use_inf
     int32_t newly_n, flag, pad0, pad1;
