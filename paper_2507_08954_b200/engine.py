@@ -528,6 +528,38 @@ def _device_cfgs(devices):
     return cfgs
 
 
+# gfq.h per-simulation statuses that are the engine's own capacity limits,
+# not the reference's behaviour: re-run with larger buffers / budget
+_SIM_EVENT_OVERFLOW, _SIM_WATCHDOG, _SIM_OUTPUT_OVERFLOW = 1, 3, 5
+
+
+def _run_one(eng: "Engine", sim, n_arrivals: int, outputs: int, early_exit: bool, **kw):
+    """One simulation through ``eng``.  The reference has no event-pool,
+    audit-buffer or event-budget limits, so a simulation that hits one of the
+    engine's is re-run with 4x the capacity (16x the event budget), as
+    cli.run_experiments does for a batch; other statuses raise."""
+    from ._lib import EngineError
+    sim = _abi.Sim.from_buffer_copy(sim)
+    for attempt in range(6):
+        eng.prepare([sim], outputs, early_exit, **kw)
+        eng.launch()
+        try:
+            eng.synchronize()
+            return BatchResult(eng)
+        except EngineError:
+            st = int(eng.output(_abi.OUT_STATUS)[0])
+            if attempt == 5 or st not in (_SIM_EVENT_OVERFLOW, _SIM_WATCHDOG, _SIM_OUTPUT_OVERFLOW):
+                raise
+        if st == _SIM_EVENT_OVERFLOW:
+            kw["event_capacity"] = max(1024, 4 * int(kw.get("event_capacity", 0)))
+        elif st == _SIM_WATCHDOG:
+            sim.max_events = 16 * (int(sim.max_events) or 64 * (n_arrivals + 1024))
+        else:
+            for k in ("audit_util_cap", "audit_backlog_cap", "event_log_cap"):
+                kw[k] = 4 * int(kw.get(k, 0) or (1 << 16))
+    raise AssertionError("unreachable")
+
+
 def run_simulation(trace, profiles, policy, devices, tau_includes_overheads: bool = False,
                    *, device: int = 0) -> SimResult:
     """Drop-in for gpufairq.engine.run_simulation (engine.py:214-218), run by
@@ -541,8 +573,8 @@ def run_simulation(trace, profiles, policy, devices, tau_includes_overheads: boo
     eng.upload_flowtabs([tab])
     eng.upload_device_cfgs(dcfgs)
     sim = sim_params(policy.kind, cfg, len(dcfgs), tau_includes_overheads=tau_includes_overheads)
-    res = eng.run([sim], outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
-                  _abi.WANT_AUDIT, early_exit=True)
+    res = _run_one(eng, sim, pt.n, _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
+                   _abi.WANT_AUDIT, True)
     out = to_sim_result(res, 0, pt)
     log = getattr(policy, "dispatch_log", None)
     if isinstance(log, list):
@@ -595,9 +627,9 @@ class Simulation:
         sim = sim_params(self.policy.kind, cfg, len(dcfgs),
                          tau_includes_overheads=self.tau_includes_overheads)
         cap = 64 * (pt.n + 1024)
-        res = eng.run([sim], outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
-                      _abi.WANT_AUDIT | _abi.WANT_EVENTS, early_exit=False, event_log_cap=cap,
-                      audit_util_cap=cap, audit_backlog_cap=2 * pt.n + 2)
+        res = _run_one(eng, sim, pt.n, _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
+                       _abi.WANT_AUDIT | _abi.WANT_EVENTS, False, event_log_cap=cap,
+                       audit_util_cap=cap, audit_backlog_cap=2 * pt.n + 2)
         self._result = to_sim_result(res, 0, pt)
         rec = res.records(0)
         for p, inv in enumerate(self._inv):

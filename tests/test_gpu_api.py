@@ -161,3 +161,37 @@ def test_trace_upload_validation_on_gpu():
         up(a3, fl)
     up(np.concatenate([good, good, good]), fl)            # a valid upload still works
     eng.close()
+
+
+def test_capacity_statuses_are_retried():
+    """The engine's event pool, audit buffers and event budget are its own
+    limits (the reference has none): a single simulation that hits one is
+    re-run with larger ones and then matches the oracle."""
+    import numpy as np
+    from oracle import oracle as orc
+    from test_gpu_fuzz import _workload
+    from paper_2507_08954_b200 import _abi
+    from paper_2507_08954_b200.engine import Engine, _run_one
+    traces, tabs, dcfgs, sims, _ = _workload(np.random.default_rng(5), 5)
+    eng = Engine(0)
+    eng.upload_traces(traces)
+    eng.upload_flowtabs(tabs)
+    eng.upload_device_cfgs(dcfgs)
+    s = sims[0]                                              # MQFQ
+    tr, tab = traces[0], tabs[0]
+    r = orc.run_packed(_abi.Sim.from_buffer_copy(s), tr.arrival, tr.flow, tr.n_flows,
+                       {"warm": tab.warm, "cold": tab.cold, "mem": tab.mem,
+                        "share": tab.share, "weight": tab.weight},
+                       [_abi.device_cfg_from(d) for d in dcfgs[s.device_cfg: s.device_cfg + s.n_devices]],
+                       want_audit=False)
+    outs = _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH | _abi.WANT_AUDIT
+    tight = _abi.Sim.from_buffer_copy(s)
+    tight.max_events = 500
+    for sim, kw in ((s, {"event_capacity": 2}), (s, {"audit_util_cap": 256}), (tight, {})):
+        res = _run_one(eng, sim, tr.n, outs, True, **kw)
+        comp = res.completion_order(0)
+        assert int(res.status[0]) == 0
+        assert np.array_equal(comp, r["rec_inv"])
+        assert np.array_equal(res.records(0)["complete"][comp], r["rec_complete"])
+        assert np.array_equal(res.dispatch_rows(0)["vt_before"], r["d_vt_before"])
+    eng.close()
