@@ -322,6 +322,7 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA, FG>& w, const Par
             for (int k = 0; k < DV_NSTATE; k++) w.hv[k] = dvi[k];
 #pragma unroll
             for (int k = 0; k < DD_NSTATE; k++) w.hd[k] = dvd[k];
+            w.win0 = dvd[DD_WINDOW];
         }
     }
     w.period = 0.0;

@@ -191,8 +191,10 @@ FI Arg warp_argmin(Arg a) {
     r.i = (int)wmin32(a.k == r.k && a.s == r.s ? (unsigned)a.i : 0x7fffffffu);
     return r;
 }
-// named barrier over the n threads of the simulation's CTA
-FI void cta_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// named barrier over the n threads of the simulation's CTA.  The non-.aligned
+// form: a warp may reach it with its lanes not yet reconverged (after the
+// lane-0 command writes), which bar.sync (= barrier.sync.aligned) forbids.
+FI void cta_bar(int id, int n) { asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // CTA = one simulation per CTA (large flow counts): warp 0
 // (the leader) runs everything below; the O(F) flow scans and the event-pool
@@ -233,6 +235,7 @@ struct WarpSim {
     FI uint32_t* ev_meta() const { return (uint32_t*)(fe + P.L.o_ev_meta); }
     // per-device fields; in the 1-device build the mutable ones are registers
     int hv[DV_NSTATE]; double hd[DD_NSTATE];
+    double win0;                       // 1-device build: device 0's util_window_s (read every tick)
     FI int& DV(int d, int k) {
         if (ND1 && k < DV_NSTATE) return hv[k];
         return ((int*)(sm + P.L.o_dvi))[d * DV_NI + k];
@@ -897,7 +900,7 @@ struct WarpSim {
         SMPT(d, w) = now; SMPU(d, w) = util;
         double oldt = ns == 0 ? now : DD(d, DD_OLDT);    // time of the oldest sample
         ns++;
-        double horizon = now - DD(d, DD_WINDOW);
+        double horizon = now - (ND1 ? win0 : DD(d, DD_WINDOW));
         #pragma unroll 1
         while (ns > 0 && oldt <= horizon) {
             head++; if (head >= S) head = 0; ns--;
