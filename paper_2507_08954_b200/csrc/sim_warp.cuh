@@ -931,7 +931,10 @@ struct WarpSim {
                 #pragma unroll 1
                 for (int k = 0; k < ns; k++) { ps_add(a, SMPU(d, j)); j++; if (j >= S) j = 0; }
                 avg = ps_val(a) / (double)ns;
-                if (memo) { USYNC(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
+                // a real barrier here (memo misses only): the slot may be
+                // rewritten a few ticks later with no warp collective in
+                // between, and racecheck cannot see convergence as ordering
+                if (memo) { __syncwarp(); WKEY(d, slot) = key; WVAL(d, slot) = avg; }
             }
             const bool dyn = DV(d, DV_DYN);
             // a fixed D and an unchanged average leave effective_d and the
