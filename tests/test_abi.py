@@ -43,6 +43,8 @@ def test_header_constants_match_abi():
     assert int(consts["GFQ_POLICY_SJF"]) == _abi.POLICY_SJF
     assert int(consts["GFQ_ABI_VERSION"]) == _abi.ABI_VERSION
     assert int(consts["GFQ_WANT_EVENTS"].rstrip("u"), 16) == _abi.WANT_EVENTS
+    for nm in ("FLOWS_GLOBAL", "CTA", "WARP"):
+        assert int(consts["GFQ_FLAG_" + nm].rstrip("u"), 16) == getattr(_abi, "FLAG_" + nm)
     enum = re.search(r"enum gfq_output_id \{(.*?)\};", src, re.S).group(1)
     names = re.findall(r"(GFQ_OUT_[A-Z_]+)", enum)
     assert names.index("GFQ_OUT_HIST") == _abi.OUT_HIST
