@@ -398,8 +398,12 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
 #define GFQ_KTHREADS 128
 #endif
 
+#ifndef GFQ_MINB_FG                       // flows-in-global builds (L2-latency bound)
+#define GFQ_MINB_FG GFQ_MINB
+#endif
+
 template <int POL, bool ND1, bool FG>
-__global__ void __launch_bounds__(GFQ_KTHREADS, GFQ_MINB) k_sim(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(GFQ_KTHREADS, FG ? GFQ_MINB_FG : GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* slice = smem + (size_t)warp * p.L.bytes;
