@@ -1478,8 +1478,8 @@ struct WarpSim {
             // at +inf (tick_t / pmin_t invariants), and with neither present and
             // no arrival left the loop has ended above, so no +inf tie remains.
             int kind; double t;
-            if (t_arr <= tick_t && t_arr <= pmin_t && t_arr != INF) { kind = EV_ARRIVAL; t = t_arr; }
-            else if (tick_t < pmin_t || (tick_t == pmin_t && tick_seq < pmin_seq)) { kind = EV_TICK; t = tick_t; }
+            if ((t_arr <= tick_t) & (t_arr <= pmin_t) & (t_arr != INF)) { kind = EV_ARRIVAL; t = t_arr; }
+            else if ((tick_t < pmin_t) | ((tick_t == pmin_t) & (tick_seq < pmin_seq))) { kind = EV_TICK; t = tick_t; }
             else { kind = 4; t = pmin_t; }
             if (UNLIKELY(n_events >= max_events)) { fail(GFQ_SIM_WATCHDOG); break; }
             now = t;
@@ -1519,13 +1519,14 @@ struct WarpSim {
                     diag(DG_TICKS);
                     log_event(now, EV_TICK, -1);
                     on_monitor();
-                    const bool quiet = q_gvt && (!MQFQ || now < idle_lb) &&
-                                       (q_idle || (q_busy && certain_refusal()));
-                    if (UNLIKELY(status) || !quiet) break;
+                    // bitwise, not short-circuit: one branch per test
+                    const bool quiet = q_gvt & (!MQFQ | (now < idle_lb)) &
+                                       (q_idle | (q_busy & certain_refusal()));
+                    if ((status != 0) | !quiet) break;
                     n_calls++;
                     diag(DG_QUIET);
                     dr = false;
-                    if (!tick_on || UNLIKELY(n_events >= max_events) || tick_t >= lim) break;
+                    if (!tick_on | (n_events >= max_events) | (tick_t >= lim)) break;
                     now = tick_t;
                     n_events++;
                     dr = true;
