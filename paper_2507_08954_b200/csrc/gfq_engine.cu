@@ -36,6 +36,9 @@
 #include "fairness.cuh"
 #include "tracegen.cuh"
 
+#ifndef GFQ_CTA_MIN
+#define GFQ_CTA_MIN 256     // CTA builds: scans shorter than this stay on the leader warp (C4: 64 -> 256 +1%)
+#endif
 #ifndef GFQ_TIMELINE
 #define GFQ_TIMELINE 0      // diagnostic build: per-simulation start/end time and SM in the counters
 #endif
@@ -623,7 +626,7 @@ struct gfq_handle {
     gfq_launch_cfg cfg{};
     Layout L{};
     int wpb = 0, rwpb = 4, rblocks = 1;
-    int cta_threads = 0, cta_min = 64;
+    int cta_threads = 0, cta_min = GFQ_CTA_MIN;
     bool rglobal = false;
     int ccount[NCLASS] = {0}, cblocks[NCLASS] = {0};   // per kernel class
     Layout Lk[NCLASS] = {};                              // per-class workspace layout
@@ -1279,7 +1282,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     h->L = L;
     h->wpb = wpb;
     h->cta_threads = cta_threads;
-    h->cta_min = (c.flags & GFQ_FLAG_CTA) ? 0 : 64;
+    h->cta_min = (c.flags & GFQ_FLAG_CTA) ? 0 : GFQ_CTA_MIN;
     h->rwpb = rwpb;
     h->rblocks = rblocks;
     h->rglobal = rglobal;
