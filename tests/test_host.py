@@ -76,3 +76,41 @@ def test_hist_bin_edges():
     b = hist_bin([0.0, 1e-3, 0.01, 1.0, 1e5, 1e9], 1e-2, 1e5, 64)
     assert b[0] == 0 and b[1] == 0 and b[2] == 0 and b[-1] == 63 and b[-2] == 63
     assert 0 < b[3] < 63
+
+
+def test_capacity_retry_policy_without_a_gpu(monkeypatch):
+    """engine._run_one (run_simulation / Simulation): the engine's own capacity
+    statuses are re-run with larger buffers; anything else raises at once."""
+    import numpy as np
+    from paper_2507_08954_b200 import _abi, engine
+    from paper_2507_08954_b200._lib import EngineError
+
+    class FakeEngine:
+        def __init__(self, statuses):
+            self.statuses, self.calls = list(statuses), []
+
+        def prepare(self, sims, outputs, early_exit, **kw):
+            self.calls.append((int(sims[0].max_events), dict(kw)))
+
+        def launch(self):
+            pass
+
+        def synchronize(self):
+            self.st = self.statuses.pop(0)
+            if self.st:
+                raise EngineError("simulation 0 failed")
+
+        def output(self, oid):
+            return np.array([self.st], dtype=np.int32)
+
+    sim = _abi.Sim()
+    eng = FakeEngine([1, 3, 5, 0])
+    monkeypatch.setattr(engine, "BatchResult", lambda e: "ok")   # no device outputs here
+    assert engine._run_one(eng, sim, 100, _abi.WANT_STATS, True, audit_util_cap=8) == "ok"
+    (m0, k0), (m1, k1), (m2, k2), (m3, k3) = eng.calls
+    assert k1["event_capacity"] == 1024                   # event-pool overflow: larger pool
+    assert m2 == 16 * 64 * (100 + 1024)                   # watchdog: 16x the event budget
+    assert k3["audit_util_cap"] == 32 and k3["event_log_cap"] == 4 << 16   # output overflow
+    bad = FakeEngine([4])                                  # past event: the reference's error
+    with pytest.raises(EngineError):
+        engine._run_one(bad, sim, 100, _abi.WANT_STATS, True)
