@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define GFQ_ABI_VERSION 1
+#define GFQ_ABI_VERSION 2
 
 /* ---- status codes ---------------------------------------------------- */
 #define GFQ_OK        0
@@ -119,11 +119,13 @@ typedef struct gfq_sim {
 #define GFQ_WANT_AUDIT     0x08u  /* AuditLog backlog/util rows (engine.py:26-37)                */
 #define GFQ_WANT_EVENTS    0x10u  /* processed-event log, Simulation.step() (engine.py:99-113)   */
 #define GFQ_WANT_HIST      0x20u  /* per-(group, flow) log-binned latency histograms             */
+#define GFQ_WANT_EVICTIONS 0x40u  /* Device.eviction_log rows (device.py:92,172,177,275)         */
 
 typedef struct gfq_launch_cfg {
     uint32_t outputs;           /* GFQ_WANT_* mask                                     */
     int32_t  early_exit;        /* 1: stop once only expiry rechecks remain (exact for
-                                   every output except GFQ_WANT_EVENTS)     */
+                                   every output except GFQ_WANT_EVENTS and
+                                   GFQ_WANT_EVICTIONS, which turn it off) */
     int32_t  event_capacity;    /* dynamic-event slots per sim, 0 = auto               */
     int32_t  sample_capacity;   /* util-sample slots per device, 0 = auto              */
     int64_t  audit_util_cap;    /* util rows per sim (GFQ_WANT_AUDIT)                  */
@@ -195,6 +197,11 @@ enum gfq_output_id {
                                   qualified-set hash, hi flow, lo flow, violated */
     GFQ_OUT_FAIR_OFF,          /* int64  [sims+1] window-row offset of each sim  */
     GFQ_OUT_FAIR_COUNT,        /* int64  [sims][3]: windows, comparable, violated */
+    GFQ_OUT_EVICT_TIME,        /* double [invocations] eviction time, the sim's
+                                  rows from its record offset in log order
+                                  (GFQ_WANT_EVICTIONS; rows <= arrivals)         */
+    GFQ_OUT_EVICT_META,        /* int32  [invocations] flow << 4 | device         */
+    GFQ_OUT_EVICT_COUNT,       /* int64  [sims]                                   */
     GFQ_OUT_COUNT_
 };
 
@@ -288,8 +295,10 @@ int  gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t ca
  * (one per active simulation class + the reducer), info[1] simulations per
  * CTA class mode (0 = warp per simulation, else CTA threads per simulation),
  * info[2] flows in global scratch (0/1), info[3] simulation warps per CTA in
- * warp mode, info[4] CTAs of the largest simulation launch.  n = entries
- * wanted (<= 5). */
+ * warp mode, info[4] CTAs of the largest simulation launch, info[5] the
+ * dynamic-event capacity per simulation actually used (slots; callers that
+ * re-run a GFQ_SIM_EVENT_OVERFLOW simulation grow from this).  n = entries
+ * wanted (<= 6). */
 int  gfq_batch_info(gfq_handle* h, int32_t* info, int32_t n);
 
 /* Output access. */

@@ -100,6 +100,11 @@ def case_inputs(case: dict):
     if "default" in prof:
         args = prof["default"]
         profiles = default_profiles(*args)
+    elif "c4" in prof:        # tests/golden/cases.c4x_case: sweep.c4's memory table
+        mems = [256.0, 512.0, 1024.0, 1500.0, 3000.0]
+        base = default_profiles(*prof["c4"])
+        profiles = {nm: FunctionProfile(nm, p.warm_exec_s, p.cold_exec_s, mems[i % 5], 0.38, 1.0)
+                    for i, (nm, p) in enumerate(base.items())}
     else:
         profiles = {row[0]: FunctionProfile(*row) for row in prof["explicit"]}
     tr = case["trace"]

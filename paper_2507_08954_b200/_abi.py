@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 GFQ_OK, GFQ_EINVAL, GFQ_ERUNTIME, GFQ_ECUDA, GFQ_ENOMEM = 0, 1, 2, 3, 4
 
 POLICY_MQFQ, POLICY_FCFS, POLICY_BATCH, POLICY_SJF, POLICY_FCFS_NAIVE = 0, 1, 2, 3, 4
@@ -31,8 +31,8 @@ SIM_STATUS = {
     7: "bad simulation parameters",
 }
 
-WANT_STATS, WANT_RECORDS, WANT_DISPATCH, WANT_AUDIT, WANT_EVENTS, WANT_HIST = (
-    0x01, 0x02, 0x04, 0x08, 0x10, 0x20)
+WANT_STATS, WANT_RECORDS, WANT_DISPATCH, WANT_AUDIT, WANT_EVENTS, WANT_HIST, WANT_EVICTIONS = (
+    0x01, 0x02, 0x04, 0x08, 0x10, 0x20, 0x40)
 
 (OUT_STATUS, OUT_COUNTERS, OUT_FINAL_TIME, OUT_SUMMARY, OUT_FLOW_COUNT,
  OUT_FLOW_MEAN, OUT_FLOW_VAR, OUT_FLOW_COLD_PCT, OUT_REC_DISPATCH,
@@ -41,7 +41,8 @@ WANT_STATS, WANT_RECORDS, WANT_DISPATCH, WANT_AUDIT, WANT_EVENTS, WANT_HIST = (
  OUT_UTIL_ROWS, OUT_UTIL_META, OUT_BACKLOG_TIME, OUT_BACKLOG_META,
  OUT_BACKLOG_COUNT, OUT_EVENT_TIME, OUT_EVENT_META, OUT_EVENT_COUNT,
  OUT_HIST, OUT_FAIR_ROWS, OUT_FAIR_META, OUT_FAIR_OFF, OUT_FAIR_COUNT,
- OUT_COUNT_) = range(33)
+ OUT_EVICT_TIME, OUT_EVICT_META, OUT_EVICT_COUNT,
+ OUT_COUNT_) = range(36)
 
 
 class DeviceCfg(C.Structure):

@@ -73,6 +73,7 @@ def run_experiments(exps: list[Experiment], device: int = 0, write: bool = True)
     traces, tabs, dcfgs = [], [], []
     trace_ix: dict[int, int] = {}
     tab_ix: dict[tuple, int] = {}
+    alive = []      # the id()-keyed objects stay alive, so no id is reused
     for e in exps:
         cfg = e.cfg
         profiles = e.profiles if e.profiles is not None else cfg.build_profiles()
@@ -80,6 +81,7 @@ def run_experiments(exps: list[Experiment], device: int = 0, write: bool = True)
         sched = cfg.scheduler_config()
         pool = cfg.pool_enabled and not PolicyKind(cfg.policy).pool_disabled
         devs = cfg.device_configs(pool_enabled=pool)
+        alive.append((trace, profiles))
         if id(trace) not in trace_ix:
             trace_ix[id(trace)] = len(traces)
             traces.append(pack_trace(trace.entries, profiles))
@@ -143,7 +145,8 @@ def run_experiments(exps: list[Experiment], device: int = 0, write: bool = True)
         if any(st[j] == _RETRY_OUTPUT for j in over):
             cap *= 8
         if any(st[j] == _RETRY_EVENTS for j in over):
-            ev_cap = (1024, 4096, 8192, 8192)[attempt]
+            # grow from the capacity that overflowed (never retry a smaller one)
+            ev_cap = 4 * eng.batch_info()["event_capacity"]
         todo = [todo[j] for j in over]
     if write:
         for (e, _, _, _), o in zip(items, outcomes):

@@ -347,6 +347,7 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA, FG>& w, const Par
     w.idle_lb = __longlong_as_double(0x7ff0000000000000ll);
     w.n_events = 0;
     w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
+    w.n_evict = 0;
     ps_init(w.util_sum);
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first
@@ -375,6 +376,7 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA, FG>& w, const Par
         p.final_time[sid] = w.now;
         if (p.outputs & GFQ_WANT_AUDIT) p.backlog_count[sid] = w.n_backlog;
         if (p.outputs & GFQ_WANT_EVENTS) p.event_count[sid] = w.n_evlog;
+        if (p.outputs & GFQ_WANT_EVICTIONS) p.evict_count[sid] = w.n_evict;
         if ((p.outputs & GFQ_WANT_AUDIT) && !w.status &&
             (w.n_backlog > p.audit_backlog_cap || w.n_util > p.audit_util_cap))
             p.status[sid] = GFQ_SIM_OUTPUT_OVERFLOW;
@@ -654,7 +656,8 @@ static const int32_t kOutBytes[GFQ_OUT_COUNT_] = {
     8, 4, 8, 4, 8,            // util rows/meta, backlog time/meta/count
     8, 8, 8,                  // event time/meta/count
     8,                        // hist
-    8, 8, 8, 8};              // fairness rows/meta/offsets/counts
+    8, 8, 8, 8,               // fairness rows/meta/offsets/counts
+    8, 4, 8};                 // eviction log time/meta/count
 
 extern "C" {
 
@@ -1121,7 +1124,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     //   1 MQFQ-Sticky on a multi-device DeviceSet
     //   2..5 one policy (MQFQ / FCFS / Batch / SJF) on a 1-device DeviceSet
     //        (flows in global scratch: MQFQ / FCFS only)
-    const bool logs = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS)) != 0;
+    const bool logs = (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS | GFQ_WANT_EVICTIONS)) != 0;
     std::vector<int> cls(n_sims);
     int ccount[NCLASS] = {0};
     for (int i = 0; i < n_sims; i++) {
@@ -1249,6 +1252,10 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
             (rc = alloc_out(h, GFQ_OUT_BACKLOG_COUNT, n_sims)))
             return rc;
     }
+    if (c.outputs & GFQ_WANT_EVICTIONS)
+        if ((rc = alloc_out(h, GFQ_OUT_EVICT_TIME, recs)) || (rc = alloc_out(h, GFQ_OUT_EVICT_META, recs)) ||
+            (rc = alloc_out(h, GFQ_OUT_EVICT_COUNT, n_sims)))
+            return rc;
     if (c.outputs & GFQ_WANT_EVENTS) {
         if (c.event_log_cap <= 0) c.event_log_cap = 64 * (int64_t)max_n + 1024;
         if ((rc = alloc_out(h, GFQ_OUT_EVENT_TIME, (int64_t)n_sims * c.event_log_cap)) ||
@@ -1348,6 +1355,9 @@ static Params make_params(gfq_handle* h) {
     p.event_meta = h->out[GFQ_OUT_EVENT_META].as<int64_t>();
     p.event_count = h->out[GFQ_OUT_EVENT_COUNT].as<int64_t>();
     p.event_log_cap = h->cfg.event_log_cap;
+    p.evict_time = h->out[GFQ_OUT_EVICT_TIME].as<double>();
+    p.evict_meta = h->out[GFQ_OUT_EVICT_META].as<int32_t>();
+    p.evict_count = h->out[GFQ_OUT_EVICT_COUNT].as<int64_t>();
     p.hist = h->out[GFQ_OUT_HIST].as<unsigned long long>();
     p.hist_rows = h->cfg.hist_rows; p.hist_bins = h->cfg.hist_bins;
     p.hist_lo = h->cfg.hist_lo_s; p.hist_hi = h->cfg.hist_hi_s;
@@ -1474,8 +1484,8 @@ int gfq_kernel_times(gfq_handle* h, float* sim_ms, float* reduce_ms, int32_t cap
 }
 
 int gfq_batch_info(gfq_handle* h, int32_t* info, int32_t n) {
-    if (!h || !h->prepared || !info || n < 0 || n > 5) return set_err(GFQ_EINVAL, "gfq_batch_info: bad arguments");
-    int32_t v[5] = {0, h->L.cta ? h->cta_threads : 0, h->L.flows_global, h->wpb, 0};
+    if (!h || !h->prepared || !info || n < 0 || n > 6) return set_err(GFQ_EINVAL, "gfq_batch_info: bad arguments");
+    int32_t v[6] = {0, h->L.cta ? h->cta_threads : 0, h->L.flows_global, h->wpb, 0, h->L.E};
     for (int k = 0; k < NCLASS; k++)
         if (h->ccount[k]) { v[0]++; v[4] = std::max(v[4], h->cblocks[k]); }
     if (h->n_sims > 0) v[0]++;                             // k_reduce

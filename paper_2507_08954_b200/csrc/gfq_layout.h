@@ -128,6 +128,7 @@ struct Params {
     double* util_rows; int32_t* util_meta; int64_t audit_util_cap;
     double* backlog_time; int32_t* backlog_meta; int64_t* backlog_count; int64_t audit_backlog_cap;
     double* event_time; int64_t* event_meta; int64_t* event_count; int64_t event_log_cap;
+    double* evict_time; int32_t* evict_meta; int64_t* evict_count;   // at the sim's record offset
     unsigned long long* hist; int32_t hist_rows, hist_bins; double hist_lo, hist_hi;
     int32_t* work;                 // work-queue counter
     double* rscratch;              // reducer: per-warp record scratch (rscratch_per_warp doubles)

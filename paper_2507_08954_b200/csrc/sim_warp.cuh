@@ -383,6 +383,7 @@ struct WarpSim {
     double idle_lb;                    // (B) no keep-alive can expire before this
     int n_events;
     int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog;
+    int n_evict;                       // Device.eviction_log rows (generic build)
     PySum util_sum;
 
     FI WarpSim(const Params& p, unsigned char* s, unsigned char* f, int l, int id)
@@ -653,8 +654,10 @@ struct WarpSim {
             ust(PM(d, v), m | (1u << 27));                 // tentatively HOST_WARM
             free_mb += mem(pm_fn(m));
             nsw++;
+            if (G) evict_log(d, pm_fn(m));                 // eviction_log.append, in victim order
         }
         bool ok = free_mb >= needed;
+        if (G && !ok) n_evict -= nsw;                      // rollback pops them (device.py:175-177)
         if (nsw) {   // commit (-> HOST_WARM) or roll back, one entry at a time
             #pragma unroll 1
             for (int base = 0; base < np; base += 32) {
@@ -1226,10 +1229,49 @@ struct WarpSim {
         if (G) __syncwarp();
     }
 
+    // Device.eviction_log row (device.py:92): lane 0 writes (now, device, flow)
+    // at the simulation's record offset (evictions <= completions: a container
+    // turns GPU_WARM only when an invocation completes into the pool)
+    FI void evict_log(int d, int fn) {
+        const int k = n_evict++;
+        if ((P.outputs & GFQ_WANT_EVICTIONS) && lane == 0) {
+            const int64_t o = P.sim_roff[sid] + k;
+            P.evict_time[o] = now; P.evict_meta[o] = (fn << 4) | d;
+        }
+    }
+    // Device.swap_out's log rows (device.py:270-275) for this call's newly
+    // inactive flows: per function (ascending: one refresh_states pass, or
+    // the single expiring flow), per device, GPU_WARM entries in pool order.
+    // Enumerated by repeated warp argmin over (device, flow, pool index).
+    FI void swap_out_log() {
+        #pragma unroll 1
+        for (int d = 0; d < NDEV(); d++) {
+            const int np = DV(d, DV_NP);
+            u64 last = 0; bool first = true;
+            #pragma unroll 1
+            while (true) {
+                u64 bk = ~0ull;
+                #pragma unroll 1
+                for (int i = lane; i < np; i += 32) {
+                    const uint32_t m = PM(d, i);
+                    if (pm_th(m) == GFQ_GPU_WARM && (fst()[pm_fn(m)] & FL_NEWLY)) {
+                        const u64 k = ((u64)pm_fn(m) << 32) | (u64)i;
+                        if ((first || k > last) && k < bk) bk = k;
+                    }
+                }
+                const u64 mk = wmin64(bk);
+                if (mk == ~0ull) break;
+                evict_log(d, (int)(mk >> 32));
+                last = mk; first = false;
+            }
+        }
+    }
+
     // _swap_out_inactive, engine.py:199-203 (+ Device.swap_out / mark_evictable)
     FI void swap_out_inactive() {
         if (LIKELY(!any_newly)) return;
         any_newly = false;
+        if (G && (P.outputs & GFQ_WANT_EVICTIONS)) swap_out_log();
         #pragma unroll 1
         for (int d = 0; d < NDEV(); d++) {
             int np = DV(d, DV_NP);
@@ -1463,7 +1505,8 @@ struct WarpSim {
         const double INF = __longlong_as_double(0x7ff0000000000000ll);
         if (RING) ring_start();
         double t_arr = n > 0 ? (RING ? ring_t(0) : arr(0)) : INF;
-        const bool early = P.early_exit && !(G && (P.outputs & GFQ_WANT_EVENTS));
+        // trailing keep-alive expiries still log events and swap-out evictions
+        const bool early = P.early_exit && !(G && (P.outputs & (GFQ_WANT_EVENTS | GFQ_WANT_EVICTIONS)));
         #pragma unroll 1
         for (;;) {
             if (!pmin_ok) pool_min();

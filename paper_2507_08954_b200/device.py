@@ -57,12 +57,15 @@ class DToken:
 
 
 class Device:
-    """Host view of one modeled GPU: its index and config.  Its mutable
-    state (pool, running set, util samples) exists only in the kernel."""
+    """Host view of one modeled GPU: its index, config and eviction log
+    (device.py:92; run_simulation / Simulation append each run's rows).  Its
+    other mutable state (pool, running set, util samples) exists only in the
+    kernel."""
 
     def __init__(self, index: int, cfg: DeviceConfig):
         self.index = index
         self.cfg = cfg
+        self.eviction_log: list[tuple[float, str]] = []
 
 
 class DeviceSet:

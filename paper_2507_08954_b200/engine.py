@@ -44,7 +44,8 @@ _OUT_DTYPES = {
     _abi.OUT_BACKLOG_COUNT: np.int64, _abi.OUT_EVENT_TIME: np.float64,
     _abi.OUT_EVENT_META: np.int64, _abi.OUT_EVENT_COUNT: np.int64, _abi.OUT_HIST: np.uint64,
     _abi.OUT_FAIR_ROWS: np.float64, _abi.OUT_FAIR_META: np.int64, _abi.OUT_FAIR_OFF: np.int64,
-    _abi.OUT_FAIR_COUNT: np.int64,
+    _abi.OUT_FAIR_COUNT: np.int64, _abi.OUT_EVICT_TIME: np.float64,
+    _abi.OUT_EVICT_META: np.int32, _abi.OUT_EVICT_COUNT: np.int64,
 }
 
 _POLICY = {"mqfq": _abi.POLICY_MQFQ, "fcfs": _abi.POLICY_FCFS, "batch": _abi.POLICY_BATCH,
@@ -257,10 +258,11 @@ class Engine:
 
     def batch_info(self) -> dict:
         """gfq_batch_info of the staged batch."""
-        v = np.zeros(5, dtype=np.int32)
-        check(self._L.gfq_batch_info(self._h, _ptr(v, C.c_int32), 5))
+        v = np.zeros(6, dtype=np.int32)
+        check(self._L.gfq_batch_info(self._h, _ptr(v, C.c_int32), 6))
         return {"launches_per_step": int(v[0]), "cta_threads": int(v[1]),
-                "flows_global": bool(v[2]), "warps_per_block": int(v[3]), "ctas": int(v[4])}
+                "flows_global": bool(v[2]), "warps_per_block": int(v[3]), "ctas": int(v[4]),
+                "event_capacity": int(v[5])}
 
     def reduce_nccl(self, comm: "NcclComm", summary_out=None, stream=None) -> None:
         """gfq_reduce_nccl: sum the last launch's latency histograms over every
@@ -447,6 +449,15 @@ class BatchResult:
         m = self.get(_abi.OUT_BACKLOG_META).reshape(-1, cap)[i, :k]
         return t, m
 
+    def eviction_rows(self, i: int):
+        """(time, device, flow) arrays of sim i's Device.eviction_log rows,
+        all devices interleaved in the order they were logged."""
+        a = int(self.rec_off[i])
+        k = int(self.get(_abi.OUT_EVICT_COUNT)[i])
+        t = self.get(_abi.OUT_EVICT_TIME)[a:a + k]
+        m = self.get(_abi.OUT_EVICT_META)[a:a + k].astype(np.int64)
+        return t, m & 15, m >> 4
+
     def event_rows(self, i: int):
         cap = self._cap(_abi.OUT_EVENT_META, 1)
         k = min(int(self.get(_abi.OUT_EVENT_COUNT)[i]), cap)
@@ -550,8 +561,8 @@ def _run_one(eng: "Engine", sim, n_arrivals: int, outputs: int, early_exit: bool
             st = int(eng.output(_abi.OUT_STATUS)[0])
             if attempt == 5 or st not in (_SIM_EVENT_OVERFLOW, _SIM_WATCHDOG, _SIM_OUTPUT_OVERFLOW):
                 raise
-        if st == _SIM_EVENT_OVERFLOW:
-            kw["event_capacity"] = max(1024, 4 * int(kw.get("event_capacity", 0)))
+        if st == _SIM_EVENT_OVERFLOW:    # grow from the capacity that overflowed
+            kw["event_capacity"] = 4 * eng.batch_info()["event_capacity"]
         elif st == _SIM_WATCHDOG:
             sim.max_events = 16 * (int(sim.max_events) or 64 * (n_arrivals + 1024))
         else:
@@ -574,12 +585,31 @@ def run_simulation(trace, profiles, policy, devices, tau_includes_overheads: boo
     eng.upload_device_cfgs(dcfgs)
     sim = sim_params(policy.kind, cfg, len(dcfgs), tau_includes_overheads=tau_includes_overheads)
     res = _run_one(eng, sim, pt.n, _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
-                   _abi.WANT_AUDIT, True)
+                   _abi.WANT_AUDIT | _abi.WANT_EVICTIONS, True)
     out = to_sim_result(res, 0, pt)
+    _share_dispatch_log(policy, out.audit)
+    _append_eviction_logs(devices, res, 0, pt.names)
+    return out
+
+
+def _append_eviction_logs(devices, res: "BatchResult", i: int, names) -> None:
+    """Device.eviction_log (device.py:92): the run's (time, function) rows
+    appended to each device's list, as the reference's devices record them."""
+    devs = list(devices)
+    t, d, f = res.eviction_rows(i)
+    for tt, dd, ff in zip(t.tolist(), d.tolist(), f.tolist()):
+        log = getattr(devs[dd], "eviction_log", None)
+        if isinstance(log, list):
+            log.append((tt, names[ff]))
+
+
+def _share_dispatch_log(policy, audit) -> None:
+    """The reference's audit.dispatches IS the policy's dispatch_log list
+    (engine.py:118): this run's rows are appended to it, earlier rows kept."""
     log = getattr(policy, "dispatch_log", None)
     if isinstance(log, list):
-        log.extend(out.audit.dispatches)
-    return out
+        log.extend(audit.dispatches)
+        audit.dispatches = log
 
 
 # event kinds, engine.py:20-23
@@ -628,9 +658,10 @@ class Simulation:
                          tau_includes_overheads=self.tau_includes_overheads)
         cap = 64 * (pt.n + 1024)
         res = _run_one(eng, sim, pt.n, _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
-                       _abi.WANT_AUDIT | _abi.WANT_EVENTS, False, event_log_cap=cap,
-                       audit_util_cap=cap, audit_backlog_cap=2 * pt.n + 2)
+                       _abi.WANT_AUDIT | _abi.WANT_EVENTS | _abi.WANT_EVICTIONS, False,
+                       event_log_cap=cap, audit_util_cap=cap, audit_backlog_cap=2 * pt.n + 2)
         self._result = to_sim_result(res, 0, pt)
+        _append_eviction_logs(self.devices, res, 0, pt.names)
         rec = res.records(0)
         for p, inv in enumerate(self._inv):
             inv.dispatch_s = float(rec["dispatch"][p])
@@ -672,10 +703,8 @@ class Simulation:
     def _finish(self) -> None:
         a = self._result.audit
         self.audit.backlog, self.audit.util, self.audit.exec = a.backlog, a.util, a.exec
+        _share_dispatch_log(self.policy, a)
         self.audit.dispatches = a.dispatches
-        log = getattr(self.policy, "dispatch_log", None)
-        if isinstance(log, list) and not log:
-            log.extend(a.dispatches)
 
     def run(self) -> SimResult:
         while self.step() is not None:

@@ -226,6 +226,45 @@ def a11_case(trial: int) -> dict:
                           "d": 1, "deny": 0, "names": names})
 
 
+C4_MEM_MB = [256.0, 512.0, 1024.0, 1500.0, 3000.0]
+
+
+def c1_cases() -> list:
+    """BASELINE C1's 10-function variant of configs/default.cfg (rate
+    3.197988, 600 s, seed 1 -> 1,875 arrivals), under every
+    policy.  default.cfg itself is appendix_b's default/* family."""
+    out = []
+    for pol in POLICIES:
+        out.append(dict(name=f"c1/f10_{pol}", trace={"gen": [10, 1.5, 3.197988, 600.0, 1]},
+                        profiles={"default": [10]}, policy=pol,
+                        sched={"t_overrun": 10.0, "alpha": 2.0},
+                        devices=[{"mem_capacity_mb": 16384.0, "d_max": 2,
+                                  "pool_max_containers": 32}]))
+    return out
+
+
+def c4x_case(idx: int) -> dict:
+    """BASELINE C4 at its full flow count (the bench's sweep.c4 profiles:
+    4096 default-profile functions, mem_mb by rank mod 5, share 0.38; Zipf
+    0.5 at 2 rps; 16 GB device, D=4, pool 32 / 256) on short traces, so the
+    reference finishes in seconds to minutes; c4x/6-7 are two of the bench's
+    own 1800 s C4 simulations (seeds 1 and 2)."""
+    dur, pol, pool, seed = [(60.0, "mqfq", 32, 101), (60.0, "mqfq", 256, 102),
+                            (60.0, "fcfs", 32, 103), (300.0, "mqfq", 32, 104),
+                            (300.0, "mqfq", 256, 105), (300.0, "fcfs", 256, 106),
+                            (1800.0, "mqfq", 32, 1), (1800.0, "fcfs", 256, 2)][idx]
+    return dict(name=f"c4x/{idx}", trace={"gen": [4096, 0.5, 2.0, dur, seed]},
+                profiles={"c4": [4096]}, policy=pol,
+                devices=[{"d_max": 4, "pool_max_containers": pool}])
+
+
+def extra_cases() -> list:
+    """Round-2 families, kept out of all_cases(): c4x's 4096-flow layout would
+    change the build the 1560-case batch runs in.  Golden file:
+    reference_golden_extra.json (make_golden.py --extra)."""
+    return c1_cases() + [c4x_case(i) for i in range(8)]
+
+
 def all_cases(n_fuzz=400, n_c3=24, n_c2=9, n_c4=4, n_a8=1000, n_a11=100):
     cases = appendix_b() + engine_cases()
     cases += [fuzz_case(i) for i in range(n_fuzz)]

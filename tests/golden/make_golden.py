@@ -23,7 +23,7 @@ REF = "/root/reference/pkg/src"
 REF_TESTS = "/root/reference/pkg/tests"
 sys.path.insert(0, HERE)
 
-from cases import all_cases  # noqa: E402
+from cases import all_cases, extra_cases  # noqa: E402
 from fingerprint import fp, hexf, per_function_rows  # noqa: E402
 
 
@@ -43,6 +43,11 @@ def ref_inputs(case):
     prof = case.get("profiles", {"default": [8]})
     if "default" in prof:
         profiles = default_profiles(*prof["default"])
+    elif "c4" in prof:        # cases.c4x_case: sweep.c4's heterogeneous-memory table
+        from cases import C4_MEM_MB
+        base = default_profiles(*prof["c4"])
+        profiles = {nm: FunctionProfile(nm, p.warm_exec_s, p.cold_exec_s, C4_MEM_MB[i % 5],
+                                        0.38, 1.0) for i, (nm, p) in enumerate(base.items())}
     else:
         profiles = {r[0]: FunctionProfile(*r) for r in prof["explicit"]}
     tr = case["trace"]
@@ -143,15 +148,24 @@ def run_reference(case):
 
 def main():
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
-    cases = all_cases()
+    # the GPU reducers replay CPython >= 3.12's compensated sum(); on 3.10 /
+    # 3.11 sum() is plain left-to-right addition and the stats would differ
+    assert sys.version_info >= (3, 12), "goldens need CPython >= 3.12 (Neumaier sum())"
+    extra = "--extra" in sys.argv
+    cases = extra_cases() if extra else all_cases()
     t0 = time.time()
     with ProcessPoolExecutor(max_workers=os.cpu_count()) as ex:
-        results = list(ex.map(run_reference, cases, chunksize=4))
+        # longest first (the 4096-flow c4x cases dominate)
+        order = sorted(range(len(cases)), key=lambda i: -len(str(cases[i])))
+        res = list(ex.map(run_reference, [cases[i] for i in order], chunksize=1 if extra else 4))
+        results = [None] * len(cases)
+        for i, r in zip(order, res):
+            results[i] = r
     out = {"generator": "tests/golden/make_golden.py",
            "reference": "gpufairq 0.1.0 (/root/reference/pkg/src, unmodified)",
            "python": sys.version.split()[0],
            "cases": results}
-    path = os.path.join(HERE, "reference_golden.json")
+    path = os.path.join(HERE, "reference_golden_extra.json" if extra else "reference_golden.json")
     with open(path, "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
     print(f"{len(results)} cases in {time.time() - t0:.0f}s -> {path}")

@@ -7,16 +7,20 @@ import os
 
 from fingerprint import fp, hexf, per_function_rows
 
-GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
-                      "reference_golden.json")
+_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+GOLDEN = os.path.join(_DIR, "reference_golden.json")
+# round-2 families (cases.extra_cases: C1's 10-function variant, C4 at 4096 flows)
+GOLDEN_EXTRA = os.path.join(_DIR, "reference_golden_extra.json")
 _cache = None
 
 
 def golden() -> dict:
     global _cache
     if _cache is None:
-        with open(GOLDEN) as fh:
-            _cache = {c["name"]: c for c in json.load(fh)["cases"]}
+        _cache = {}
+        for path in (GOLDEN, GOLDEN_EXTRA):
+            with open(path) as fh:
+                _cache.update({c["name"]: c for c in json.load(fh)["cases"]})
     return _cache
 
 

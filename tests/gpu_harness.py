@@ -15,7 +15,7 @@ from paper_2507_08954_b200.pack import FlowTable, PackedTrace
 
 STATE = ("gpu_warm", "host_warm", "cold")
 ALL_OUT = (_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH | _abi.WANT_AUDIT |
-           _abi.WANT_EVENTS)
+           _abi.WANT_EVENTS | _abi.WANT_EVICTIONS)
 
 
 def build_batch(cases):
@@ -93,7 +93,7 @@ def run_cases(cases, eng: Engine | None = None, outputs=ALL_OUT, early_exit=Fals
                          ("audit_backlog_cap", 8192)):
                 kw2[k] = int(kw.get(k, 0) or d) * 8
         if any(outs[i]["status"] == 1 for i in retry):
-            kw2["event_capacity"] = (1024, 4096, 8192)[_depth]
+            kw2["event_capacity"] = 4 * eng.batch_info()["event_capacity"]
         sub, _ = run_cases([cases[i] for i in retry], eng, outputs, early_exit, _depth + 1, **kw2)
         for i, o in zip(retry, sub):
             outs[i] = o
@@ -142,6 +142,11 @@ def normalise(res, i, case, meta, outputs):
             kind, pay = x & 3, x >> 2
             evs.append((t, kind, names[pay] if kind == 3 else (None if kind == 2 else pay)))
         out["events"] = evs
+    if outputs & _abi.WANT_EVICTIONS:
+        t, d, f = res.eviction_rows(i)
+        rows = [(float(a), int(b), names[int(c)]) for a, b, c in zip(t.tolist(), d.tolist(), f.tolist())]
+        # Device.eviction_log is per device: grouped stably by device index
+        out["evictions"] = sorted(rows, key=lambda r: r[1])
     sm = res.summary[i]
     out["summary"] = {"weighted_avg_latency_s": float(sm[0]), "cold_hit_pct": float(sm[1]),
                       "mean_util": float(sm[2])}
@@ -163,7 +168,7 @@ def close(a: float, b: float, rel=1e-9) -> bool:
 
 
 def compare_to_golden(out: dict, gold: dict, exact_keys=("dispatch", "records", "exec", "util",
-                                                         "backlog", "events")) -> list[str]:
+                                                         "backlog", "events", "evictions")) -> list[str]:
     """Bit-exact fingerprints for traces/records/audit; 1e-9 relative for the
     per-function statistics and run summary (north_star tolerance)."""
     from fingerprint import fp

@@ -22,25 +22,32 @@ def engine():
     e.close()
 
 
-def _bench_launch(eng, w):
+def _bench_launch(eng, w, flags=0):
     from paper_2507_08954_b200 import _abi, sweep
     eng.run(w.sims_array(), outputs=_abi.WANT_STATS | _abi.WANT_HIST, early_exit=True,
             hist_groups=w.groups, hist_rows=w.hist_rows, hist_bins=sweep.HIST_BINS,
-            hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S)
+            hist_lo_s=sweep.HIST_LO_S, hist_hi_s=sweep.HIST_HI_S, flags=flags)
     return {oid: eng.output(oid).copy() for oid in (
         _abi.OUT_STATUS, _abi.OUT_COUNTERS, _abi.OUT_SUMMARY, _abi.OUT_FLOW_COUNT,
         _abi.OUT_FLOW_MEAN, _abi.OUT_FLOW_VAR, _abi.OUT_FLOW_COLD_PCT, _abi.OUT_HIST)}
 
 
-def _check(eng, w, n_sample, seed=0):
+def _check(eng, w, n_sample, seed=0, flags=0, expect=None):
+    """expect: batch_info() entries the bench launch must have (its build)."""
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import oracle as orc
     from paper_2507_08954_b200 import _abi
     from paper_2507_08954_b200.engine import BatchResult
     w.upload(eng)
-    bench = _bench_launch(eng, w)
+    bench = _bench_launch(eng, w, flags)
+    info = eng.batch_info()
+    for k, v in (expect or {}).items():
+        assert info[k] == v, (k, info)
     assert (bench[_abi.OUT_STATUS] == 0).all()
     eng.run(w.sims_array(), outputs=_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH,
-            early_exit=True)
+            early_exit=True, flags=flags)
+    for k, v in (expect or {}).items():
+        assert eng.batch_info()[k] == v, (k, eng.batch_info())
     res = BatchResult(eng)
     c = res.counters
     n_arr = np.array([w.traces[s.trace].n for s in w.sims])
@@ -54,17 +61,23 @@ def _check(eng, w, n_sample, seed=0):
                 _abi.OUT_FLOW_COLD_PCT):
         assert np.array_equal(bench[oid], res.get(oid)), oid
     assert int(bench[_abi.OUT_HIST].sum()) == int(n_arr.sum())
-    # a random sample against the oracle
+    # a random sample against the oracle (ctypes releases the GIL: threads)
     rng = np.random.default_rng(seed)
     bad = []
-    for i in sorted(rng.choice(len(w.sims), n_sample, replace=False).tolist()):
+    sample = sorted(rng.choice(len(w.sims), n_sample, replace=False).tolist())
+
+    def oracle_run(i):
         s = w.sims[i]
         tr, tab = w.traces[s.trace], w.tabs[s.flowtab]
         dc = w.dcfgs[s.device_cfg: s.device_cfg + s.n_devices]
-        r = orc.run_packed(_abi.Sim.from_buffer_copy(s), tr.arrival, tr.flow, tr.n_flows,
-                           {"warm": tab.warm, "cold": tab.cold, "mem": tab.mem,
-                            "share": tab.share, "weight": tab.weight},
-                           [_abi.device_cfg_from(d) for d in dc], want_audit=False)
+        return orc.run_packed(_abi.Sim.from_buffer_copy(s), tr.arrival, tr.flow, tr.n_flows,
+                              {"warm": tab.warm, "cold": tab.cold, "mem": tab.mem,
+                               "share": tab.share, "weight": tab.weight},
+                              [_abi.device_cfg_from(d) for d in dc], want_audit=False)
+
+    with ThreadPoolExecutor(max_workers=16) as ex:
+        refs = list(ex.map(oracle_run, sample))
+    for i, r in zip(sample, refs):
         rec = res.records(i)
         comp = res.completion_order(i)
         dr = res.dispatch_rows(i)
@@ -100,3 +113,21 @@ def test_c2_sample_of_seeds(engine):
 def test_c5_shard_sample(engine):
     from paper_2507_08954_b200 import sweep
     _check(engine, sweep.build("c5", 0, engine=engine, n_seeds=48), 120, seed=2)
+
+
+def test_c4_bench_batch_cta(engine):
+    """BASELINE C4 exactly as the bench runs it: 148 simulations of 4096
+    functions (37 seeds x pool 32/256 x MQFQ/FCFS, 1800 s), one per SM on the
+    CTA-per-simulation build; 32 sampled against the oracle."""
+    from paper_2507_08954_b200 import sweep
+    _check(engine, sweep.build("c4", 0, engine=engine), 32, seed=3,
+           expect={"cta_threads": 512, "flows_global": False})
+
+
+def test_c4_large_batch_flows_global(engine):
+    """C4 at 2368 simulations (592 seeds): the batch size where gfq_prepare
+    switches to the warp build with the flow state in global scratch (16
+    simulations per SM); conservation over all 2368, 32 sampled vs the oracle."""
+    from paper_2507_08954_b200 import sweep
+    _check(engine, sweep.build("c4", 0, engine=engine, n_seeds=592), 32, seed=4,
+           expect={"cta_threads": 0, "flows_global": True})

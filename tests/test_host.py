@@ -103,12 +103,15 @@ def test_capacity_retry_policy_without_a_gpu(monkeypatch):
         def output(self, oid):
             return np.array([self.st], dtype=np.int32)
 
+        def batch_info(self):
+            return {"event_capacity": 352}                 # the auto capacity that overflowed
+
     sim = _abi.Sim()
     eng = FakeEngine([1, 3, 5, 0])
     monkeypatch.setattr(engine, "BatchResult", lambda e: "ok")   # no device outputs here
     assert engine._run_one(eng, sim, 100, _abi.WANT_STATS, True, audit_util_cap=8) == "ok"
     (m0, k0), (m1, k1), (m2, k2), (m3, k3) = eng.calls
-    assert k1["event_capacity"] == 1024                   # event-pool overflow: larger pool
+    assert k1["event_capacity"] == 4 * 352                # event-pool overflow: 4x what overflowed
     assert m2 == 16 * 64 * (100 + 1024)                   # watchdog: 16x the event budget
     assert k3["audit_util_cap"] == 32 and k3["event_log_cap"] == 4 << 16   # output overflow
     bad = FakeEngine([4])                                  # past event: the reference's error

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import pytest
 
-from cases import all_cases
+from cases import all_cases, extra_cases
 from golden_check import golden, mismatches
 
 from oracle import oracle
@@ -35,3 +35,17 @@ def test_oracle_matches_reference(family):
             bad[case["name"]] = m
     assert n > 0
     assert not bad, f"{len(bad)}/{n} cases differ: {dict(list(bad.items())[:5])}"
+
+
+@pytest.mark.parametrize("family", ["c1", "c4x"])
+def test_oracle_matches_reference_extra(family):
+    """C1's 10-function variant under every policy, and C4 at its full 4096
+    flows (short traces plus two of the bench's own 1800 s simulations)."""
+    gold = golden()
+    cases = [c for c in extra_cases() if c["name"].split("/")[0] == family]
+    bad = {}
+    for case in cases:
+        m = mismatches(oracle.run_case(case, want_events=True), gold[case["name"]])
+        if m:
+            bad[case["name"]] = m
+    assert cases and not bad, bad
