@@ -1,16 +1,25 @@
 """bench.py — simulated MQFQ-Sticky dispatch decisions per second on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gfq|reference]
-                    [--workload c3|c2]
+                    [--workload c3|c1|c1f10|c2|c4|c5] [--split weak|strong]
 
-A step is one pass of the hot path over one batch: the whole C3 sweep
-(BASELINE configs[2], the configuration the metric's "1/2/4/8 B200" and the
-north-star target are quoted on: 4096 MQFQ-Sticky simulations of a 100-flow
-Azure-shaped Zipf trace, T x alpha x D x 16 seeds) run by one k_sim launch,
-including the in-kernel per-function reducer and latency histograms, plus
-(N > 1) the NCCL all-reduce of the histograms.  Under torchrun each rank
-simulates its own disjoint block of 16 seeds (weak scaling: 4096 sims per
-GPU, no data-path collective).
+A step is one pass of the hot path over one batch: by default the whole C3
+sweep (BASELINE configs[2], the configuration the metric's "1/2/4/8 B200" and
+the north-star target are quoted on: 4096 MQFQ-Sticky simulations of a
+100-flow Azure-shaped Zipf trace, T x alpha x D x 16 seeds) run by one k_sim
+launch, including the per-function reducer and latency histograms, plus
+(N > 1) the NCCL all-reduce of the histograms and all-gather of the
+per-simulation summary rows.
+
+--split weak    (default) each rank simulates its own disjoint block of 16
+                seeds: 4096 simulations per GPU, no data-path collective.
+--split strong  the ONE fixed 4096-simulation sweep, split over the ranks by
+                an a-priori cost model (dist.partition: greedy LPT on
+                N_arrivals x F_touched); total work is fixed.
+--workload c1   BASELINE configs[0]: the reference's default run (one
+                simulation); the line adds per-simulation latencies for the
+                stats build and the records/audit build and through the
+                public run_simulation drop-in.
 
 value   successful dispatches (DispatchAudit rows) summed over all ranks /
         max-over-ranks device time of the K timed steps, inputs resident in HBM,
@@ -19,10 +28,18 @@ e2e     the same metric through the public Python API with host buffers: trace
         / flow-table / config / sim-block uploads from pinned memory, launch,
         and the device->host copy of status, counters, summary and per-function
         statistics, every step.
+roofline  SM issue (the binding roof): warp-instructions of the
+        dominant kernel per launch (from the committed ncu capture of the same
+        source build and workload, profiles/ncu_k_sim_<workload>.json) / its
+        mean launch time measured here, against 148 SMs x 4 issue slots x the
+        SM clock sampled during the run.  roofline_hbm: algorithmic bytes.
 cpu_baseline  the C oracle port (oracle/, the reference algorithm restated in
         C; ~100x faster than the reference's Python) on one host core, on a
-        bounded random sample of the same sweep.
---impl reference  the same oracle port on ALL host cores (rank 0 only).
+        bounded random sample of the same sweep, with the engine's exact early
+        exit (both arms process the same events).
+python_reference  the UNMODIFIED reference (gpufairq, baseline/_ref via
+        tools/install_ref.sh) on all host cores, on a bounded random sample.
+--impl reference  the oracle port on ALL host cores (rank 0 only).
 """
 
 from __future__ import annotations
@@ -52,7 +69,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gfq", choices=["gfq", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c1", "c1f10", "c2", "c4", "c5"])
+    ap.add_argument("--split", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--py-seconds", type=float, default=15.0,
+                    help="wall seconds of the unmodified Python reference sample (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
@@ -90,7 +110,7 @@ def _oracle_jobs(w, idxs):
 def _oracle_one(job):
     orc, sim, tr, tab, dc = job
     r = orc.run_packed(sim, tr.arrival, tr.flow, tr.n_flows, tab, dc, want_audit=False,
-                       want_dispatch=False, want_records=True, want_stats=True)
+                       want_dispatch=False, want_records=True, want_stats=True, early_exit=True)
     return len(r["rec_inv"])
 
 
@@ -114,6 +134,89 @@ def cpu_sample(w, seconds: float, threads: int, seed: int = 0):
     return done_disp, done_sims, dt
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+_PY_REF = None
+
+
+def _py_ref_init(src):
+    global _PY_REF
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    import gpufairq
+    _PY_REF = gpufairq
+
+
+def _py_ref_one(job):
+    """One simulation through the UNMODIFIED reference (engine.py:214-218)."""
+    entries, prof_rows, pol, sched, devs = job
+    from gpufairq.core import FunctionProfile
+    from gpufairq.device import DeviceConfig, DeviceSet
+    from gpufairq.engine import run_simulation
+    from gpufairq.mqfq import SchedulerConfig
+    from gpufairq.policies import make_policy
+    from gpufairq.workload import Trace
+    profiles = {r[0]: FunctionProfile(*r) for r in prof_rows}
+    trace = Trace(entries=entries, duration_s=entries[-1][0] if entries else 0.0)
+    policy = make_policy(pol, profiles, SchedulerConfig(**sched))
+    res = run_simulation(trace, profiles, policy, DeviceSet([DeviceConfig(**d) for d in devs]))
+    return len(res.audit.dispatches)
+
+
+def python_reference_sample(w, seconds: float, seed: int = 0):
+    """The unmodified Python reference (baseline/_ref, tools/install_ref.sh) on
+    random sims of the workload, one process per host core, for ~`seconds`."""
+    from concurrent.futures import ProcessPoolExecutor, as_completed
+    from dataclasses import asdict
+    src = os.path.join(ROOT, "baseline", "_ref")
+    if seconds <= 0 or not os.path.isfile(os.path.join(src, "gpufairq", "__init__.py")):
+        return None
+    names = {0: "mqfq", 1: "fcfs", 2: "batch", 3: "sjf", 4: "fcfs_naive"}
+    rng = random.Random(seed)
+    order = list(range(len(w.sims)))
+    rng.shuffle(order)
+
+    def job(i):
+        s = w.sims[i]
+        tr, tab = w.traces[s.trace], w.tabs[s.flowtab]
+        entries = [(float(t), tr.names[f]) for t, f in zip(tr.arrival.tolist(), tr.flow.tolist())]
+        rows = [(nm, float(tab.warm[k]), float(tab.cold[k]), float(tab.mem[k]),
+                 float(tab.share[k]), float(tab.weight[k])) for k, nm in enumerate(tr.names)]
+        sched = {"t_overrun": float(s.t_overrun), "alpha": float(s.alpha),
+                 "default_ttl_s": float(s.default_ttl_s)}
+        devs = [asdict(d) for d in w.dcfgs[s.device_cfg: s.device_cfg + s.n_devices]]
+        return entries, rows, names[int(s.policy)], sched, devs
+
+    cores = os.cpu_count() or 1
+    disp = sims = 0
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores, initializer=_py_ref_init, initargs=(src,)) as ex:
+        pos, live = 0, set()
+        while pos < len(order) and len(live) < 2 * cores:
+            live.add(ex.submit(_py_ref_one, job(order[pos]))); pos += 1
+        while live:
+            done = next(as_completed(live))
+            live.discard(done)
+            disp += done.result(); sims += 1
+            if time.perf_counter() - t0 < seconds and pos < len(order):
+                live.add(ex.submit(_py_ref_one, job(order[pos]))); pos += 1
+        dt = time.perf_counter() - t0
+    return {"value": disp / dt, "unit": UNIT, "cores": cores, "kind": "python",
+            "cpu_model": cpu_model(),
+            "sample": f"{sims} random sims of the {w.name} workload ({disp} dispatches, "
+                      f"{dt:.1f} s wall) through the unmodified reference run_simulation "
+                      f"(gpufairq 0.1.0, baseline/_ref), {cores} processes"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -133,12 +236,16 @@ def run_reference(args):
     v = disp / secs
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.split == "strong" else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_zipf traces, default profiles)",
             "config": dict(w.describe, parallelism=f"{threads} host threads"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "cpu_model": cpu_model(),
                              "sample": f"{sims} random sims of the {args.workload} sweep "
-                                       f"({disp} dispatches) through oracle/gfq_oracle.c"},
+                                       f"({disp} dispatches) through oracle/gfq_oracle.c "
+                                       f"with the engine's exact early exit"},
+            "python_reference": python_reference_sample(w, args.py_seconds),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,9 +317,24 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of k_sim from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_k_sim.json")
+def source_hash() -> str:
+    """Hash of the engine sources (csrc + include/gfq.h): ties an ncu capture
+    to the build it measured."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2507_08954_b200", "csrc", "*"))) + \
+        [os.path.join(ROOT, "include", "gfq.h")]
+    for f in files:
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:12]
+
+
+def ncu_capture(workload: str):
+    """The committed ncu --set full numbers of this workload's dominant
+    kernel (tools/ncu_summary.py -> profiles/ncu_k_sim_<workload>.json)."""
+    p = os.path.join(ROOT, "profiles", f"ncu_k_sim_{workload}.json")
     if os.path.exists(p):
         try:
             return json.load(open(p))
@@ -242,7 +364,16 @@ def run_gfq(args):
     # the sweep's traces come from the GPU trace generator (gfq_generate_traces,
     # bit-identical to gen_zipf); the arrays are also kept on the host for the
     # e2e leg's uploads and the CPU baseline
-    w = sweep.build(args.workload, rank, engine=eng, **({"n_seeds": args.seeds} if args.seeds else {}))
+    if args.split == "strong":
+        # ONE fixed sweep (rank 0's seeds on every rank), cost-partitioned
+        from paper_2507_08954_b200.dist import partition
+        w_full = sweep.build(args.workload, 0, engine=eng,
+                             **({"n_seeds": args.seeds} if args.seeds else {}))
+        part = partition(sweep.sim_costs(w_full), world)[rank]
+        w = sweep.restrict(w_full, part)
+    else:
+        w = sweep.build(args.workload, rank, engine=eng,
+                        **({"n_seeds": args.seeds} if args.seeds else {}))
     w.upload(eng)
     outputs = _abi.WANT_STATS | _abi.WANT_HIST
     kw = dict(hist_groups=w.groups, hist_rows=w.hist_rows, hist_bins=sweep.HIST_BINS,
@@ -340,50 +471,132 @@ def run_gfq(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    # roofline of the dominant kernel (k_sim): algorithmic bytes per launch
-    n_arr = w.arrivals
-    n_flows = int(sum(w.traces[s.trace].n_flows for s in w.sims))
-    alg_bytes = 12 * n_arr + 32 * n_flows + 76 * len(w.sims)
     kern_ms = float(statistics.mean(sim_ms)) if len(sim_ms) else statistics.mean(step_ms)
-    peak, peak_src = peaks()
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    nc = ncu_traffic()
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": (nc or {}).get("dram_bytes_per_launch"),
-            "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": alg_bytes,
-            "note": "k_sim is latency/issue-bound serial event processing; HBM is not binding",
-            "sm_issue_pct_ncu": (nc or {}).get("sm_inst_issued_pct"),
-            "ncu_capture": (nc or {}).get("capture")}
-    cpu = None
+    ck = clk.summary()
+    roof, roof_hbm = rooflines(w, args.workload, kern_ms, disp_per_step, events_per_step,
+                               calls_per_step, ck, info)
+    cpu = pyref = None
     if world == 1 and not args.no_cpu_baseline:
         import oracle.oracle as orc
         orc.build()
         d, n, dt = cpu_sample(w, args.cpu_seconds, 1)
-        cpu = {"value": d / dt, "unit": UNIT, "cores": 1, "kind": "port",
+        cpu = {"value": d / dt, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{n} random sims of the {args.workload} sweep ({d} dispatches, "
-                         f"{dt:.1f} s) through oracle/gfq_oracle.c, 1 thread"}
+                         f"{dt:.1f} s) through oracle/gfq_oracle.c, 1 thread, with the "
+                         f"engine's exact early exit"}
+        pyref = python_reference_sample(w, args.py_seconds)
+    extra = {}
+    if args.workload.startswith("c1"):
+        extra = c1_latencies(eng, w, kw, stream, flush, args.steps, step_ms)
+    strong = args.split == "strong"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (gen_zipf Azure-shaped traces, default profiles; per-rank seed blocks)",
-        "config": dict(w.describe, parallelism=f"sims sharded over {world} GPU(s), " + (
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen_zipf Azure-shaped traces, default profiles; " + (
+            "one fixed sweep cost-partitioned over the ranks)" if strong else "per-rank seed blocks)"),
+        "config": dict(w.describe, parallelism=(
+                           f"one fixed sweep LPT-partitioned over {world} GPU(s), " if strong else
+                           f"sims sharded over {world} GPU(s), ") + (
                            f"CTA ({info['cta_threads']} threads) per simulation"
                            if info["cta_threads"] else "warp per simulation"),
                        l2="flushed (256 MiB write) before every step",
                        outputs="per-function stats + latency histograms",
                        dispatch_calls_per_step=calls_per_step, events_per_step=events_per_step,
                        dispatches_per_step_per_gpu=disp_per_step, **scans),
-        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-        "clocks": clk.summary(), "gpu_launches": args.steps * info["launches_per_step"],
+        "e2e": e2e, "roofline": roof, "roofline_hbm": roof_hbm, "cpu_baseline": cpu,
+        "python_reference": pyref,
+        "clocks": ck, "gpu_launches": args.steps * info["launches_per_step"],
         "kernel_ms": {"k_sim_mean": kern_ms, "k_reduce_mean": float(statistics.mean(red_ms))
                       if len(red_ms) else None, "step_mean": statistics.mean(step_ms),
                       "step_min": min(step_ms), "step_max": max(step_ms)},
+        **extra,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def rooflines(w, workload, kern_ms, disp, events, calls, clocks, info):
+    """SM-issue roofline of the dominant kernel (the binding roof, SURVEY
+    §8(d)) plus the HBM one.  Warp-instructions per launch come from the
+    committed ncu --set full capture of the same source build and workload
+    (they are a deterministic function of build and inputs); the launch time
+    and SM clock are this run's."""
+    import torch
+    n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    nc = ncu_capture(workload) or {}
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    peak_issue = n_sm * 4 * mhz * 1e6 / 1e9          # G warp-instructions / s
+    inst = nc.get("inst_executed_per_launch")
+    same = nc.get("source_hash") == source_hash() and nc.get("sims") == len(w.sims)
+    roof = {"bound": "sm_issue", "unit": "G warp-inst/s", "peak": peak_issue,
+            "peak_source": f"{n_sm} SMs x 4 issue slots x {mhz:.0f} MHz (sampled SM clock)",
+            "achieved": None, "frac": None, "traffic": nc.get("dram_bytes_per_launch"),
+            "ncu_capture": nc.get("capture"), "ncu_same_build": bool(same)}
+    if inst:
+        a = inst / (kern_ms / 1e3) / 1e9
+        roof.update(achieved=a, frac=a / peak_issue, warp_inst_per_launch=inst,
+                    warp_inst_per_dispatch=inst / max(disp, 1),
+                    warp_inst_per_event=inst / max(events, 1),
+                    warp_inst_per_dispatch_call=inst / max(calls, 1),
+                    sm_inst_issued_pct_ncu=nc.get("sm_inst_issued_pct"),
+                    warps_active_pct_ncu=nc.get("warps_active_pct"))
+    n_arr = w.arrivals
+    n_flows = int(sum(w.traces[s.trace].n_flows for s in w.sims))
+    alg_bytes = 12 * n_arr + 32 * n_flows + 76 * len(w.sims)
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    hbm = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": achieved / peak, "traffic": nc.get("dram_bytes_per_launch"),
+           "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+           "note": "12 B per arrival + 32 B per (sim, flow) + 76 B per sim; not binding"}
+    return roof, hbm
+
+
+def c1_latencies(eng, w, kw, stream, flush, steps, stats_ms):
+    """BASELINE C1: per-simulation latency of the single default run, in the
+    stats build (the timed steps), the records / dispatch / audit / eviction
+    build (generic class), and end to end through the public run_simulation
+    drop-in (pack, upload, launch, reference-shaped results)."""
+    import torch
+    from paper_2507_08954_b200 import _abi
+    from paper_2507_08954_b200.device import DeviceConfig, DeviceSet
+    from paper_2507_08954_b200.engine import run_simulation
+    from paper_2507_08954_b200.mqfq import SchedulerConfig
+    from paper_2507_08954_b200.policies import make_policy
+    from paper_2507_08954_b200.workload import default_profiles, gen_zipf
+    rec_out = (_abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH | _abi.WANT_AUDIT |
+               _abi.WANT_EVICTIONS)
+    eng.prepare(w.sims_array(), outputs=rec_out, early_exit=True)
+    ms = []
+    for k in range(steps + 2):
+        flush.fill_(k)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream); eng.launch(stream); b.record(stream)
+        torch.cuda.synchronize()
+        if k >= 2:
+            ms.append(a.elapsed_time(b))
+    d = w.describe
+    prof = default_profiles(d["functions"])
+    trace = gen_zipf(d["functions"], d["zipf_s"], d["rate_rps"], d["duration_s"], d["seed"],
+                     names=list(prof))
+    run_simulation(trace, prof, make_policy("mqfq", prof, SchedulerConfig(10.0, 2, 2.0)),
+                   DeviceSet([DeviceConfig(d_max=2)]))
+    wall = []
+    for _ in range(steps):
+        pol = make_policy("mqfq", prof, SchedulerConfig(10.0, 2, 2.0))
+        t0 = time.perf_counter()
+        res = run_simulation(trace, prof, pol, DeviceSet([DeviceConfig(d_max=2)]))
+        wall.append(1e3 * (time.perf_counter() - t0))
+    # restore the stats launch the caller set up
+    eng.prepare(w.sims_array(), outputs=_abi.WANT_STATS | _abi.WANT_HIST, early_exit=True, **kw)
+    return {"c1_latency_ms": {
+        "stats_build_device": statistics.median(stats_ms),
+        "records_audit_build_device": statistics.median(ms),
+        "run_simulation_e2e_wall": statistics.median(wall),
+        "dispatches": len(res.records),
+        "note": "one simulation = one warp: serial event processing, ~1 us per event"}}
 
 
 class _CudaArray:

@@ -35,7 +35,11 @@ typedef struct gfq_oracle_out {
     double   weighted_avg_latency, cold_hit_pct, mean_util, final_time;
     int64_t  n_events, n_dispatch_calls;
     int32_t  status;
-    int32_t  reserved;
+    int32_t  early_exit;    /* in: 1 = stop once only keep-alive rechecks remain
+                               (no tick scheduled, every arrival processed,
+                               nothing pending or in flight): the engine's
+                               bench-launch rule (gfq_launch_cfg.early_exit),
+                               so both bench arms process the same events    */
 } gfq_oracle_out;
 
 int gfq_oracle_run(const gfq_sim* sim,

@@ -59,7 +59,7 @@ class OracleOut(C.Structure):
         ("weighted_avg_latency", C.c_double), ("cold_hit_pct", C.c_double),
         ("mean_util", C.c_double), ("final_time", C.c_double),
         ("n_events", C.c_int64), ("n_dispatch_calls", C.c_int64),
-        ("status", C.c_int32), ("reserved", C.c_int32),
+        ("status", C.c_int32), ("early_exit", C.c_int32),
     ]
 
 
@@ -137,14 +137,15 @@ def pack(entries, profiles, weights=None):
 
 def run_packed(sim: _abi.Sim, arrival, flow, n_flows, tab, devcfgs, execs=None,
                want_events=False, want_audit=True, want_dispatch=True,
-               want_records=True, want_stats=True, caps=None):
+               want_records=True, want_stats=True, caps=None, early_exit=False):
     """Run one simulation through the oracle on packed inputs; returns the
     raw numpy outputs (trace positions, flow ids, state codes).  Audit and
     event buffers grow and the run repeats when a first guess was short."""
     caps = caps or {"u": 16 * 1024, "x": 4 * 1024, "ev": 64 * 1024}
     while True:
         r = _run_packed_once(sim, arrival, flow, n_flows, tab, devcfgs, execs, want_events,
-                             want_audit, want_dispatch, want_records, want_stats, caps)
+                             want_audit, want_dispatch, want_records, want_stats, caps,
+                             early_exit)
         need = r.pop("_need")
         short = {k: v for k, v in need.items() if v > caps[k]}
         if not short:
@@ -153,9 +154,10 @@ def run_packed(sim: _abi.Sim, arrival, flow, n_flows, tab, devcfgs, execs=None,
 
 
 def _run_packed_once(sim, arrival, flow, n_flows, tab, devcfgs, execs, want_events,
-                     want_audit, want_dispatch, want_records, want_stats, caps):
+                     want_audit, want_dispatch, want_records, want_stats, caps, early_exit=False):
     n = int(arrival.shape[0])
     o = OracleOut()
+    o.early_exit = int(bool(early_exit))
     keep = []
 
     def arr(dtype, size):

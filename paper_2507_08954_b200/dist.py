@@ -23,6 +23,27 @@ def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + q + (1 if rank < r else 0)
 
 
+def partition(costs, world: int) -> list[list[int]]:
+    """Strong-scaling split of ONE fixed sweep over ``world`` ranks: greedy
+    LPT on the a-priori costs (sweep.sim_costs), longest first onto the least
+    loaded rank that still has room, every rank getting ceil/floor(n/world)
+    simulations (equal row blocks for the summary all-gather).  Each rank's
+    list is in ascending sim order.  Every rank computes the same split from
+    the same inputs, so no exchange is needed before the simulations run."""
+    if world < 1:
+        raise ValueError("bad world")
+    n = len(costs)
+    room = [shard_bounds(n, r, world)[1] - shard_bounds(n, r, world)[0] for r in range(world)]
+    order = sorted(range(n), key=lambda i: (-costs[i], i))
+    load = [0.0] * world
+    parts: list[list[int]] = [[] for _ in range(world)]
+    for i in order:
+        r = min((k for k in range(world) if len(parts[k]) < room[k]), key=lambda k: (load[k], k))
+        parts[r].append(i)
+        load[r] += costs[i]
+    return [sorted(p) for p in parts]
+
+
 def hist_bin(x, lo: float, hi: float, bins: int):
     """The reducer's latency binning (gfq_engine.cu k_reduce):
     floor((log x - log lo) * bins / (log hi - log lo)), clamped; x <= 0 -> 0."""

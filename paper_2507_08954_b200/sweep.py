@@ -205,9 +205,50 @@ def c5(seed_base: int = 1, n_traces: int = 1563, duration: float = 600.0, engine
                               "duration_s": duration, "sims": len(sims)})
 
 
+def c1(variant: str = "default", engine=None) -> Workload:
+    """BASELINE C1 (configs[0]): the reference's default run, one simulation.
+    ``default`` is configs/default.cfg verbatim (24 functions, Zipf 1.5,
+    2.69 rps, 600 s, seed 1; MQFQ-Sticky T=10, alpha=2; one 16 GB device,
+    D=2, pool 32: 1,586 arrivals); ``f10`` its 10-function variant (3.197988
+    rps -> 1,875 arrivals)."""
+    n_fn, rate = {"default": (24, 2.69), "f10": (10, 3.197988)}[variant]
+    traces, tabs = _traces(n_fn, 1.5, [(rate, 1)], 600.0, engine)
+    dcfgs = [DeviceConfig(mem_capacity_mb=16384.0, d_max=2, pool_max_containers=32)]
+    sims = [sim_params("mqfq", SchedulerConfig(t_overrun=10.0, d_max=2, alpha=2.0), 1,
+                       trace=0, flowtab=0, device_cfg=0, group=0)]
+    return Workload("c1", traces, tabs, dcfgs, sims, groups=1, hist_rows=n_fn,
+                    describe={"workload": f"C1 reference default run ({variant}): one "
+                                          "MQFQ-Sticky simulation, per-simulation latency",
+                              "functions": n_fn, "zipf_s": 1.5, "rate_rps": rate,
+                              "duration_s": 600.0, "seed": 1, "d_max": 2, "pool": 32,
+                              "sims": 1})
+
+
+def sim_costs(w: Workload) -> list[float]:
+    """A-priori cost of each simulation for partitioning (SURVEY §8(e):
+    N_arrivals x F_touched), scaled like the engine's LPT estimate by the
+    policy and the device concurrency (gfq_prepare's work order)."""
+    out = []
+    for s in w.sims:
+        tr = w.traces[s.trace]
+        d = sum(w.dcfgs[s.device_cfg + k].d_max for k in range(s.n_devices))
+        out.append(tr.n * (1.0 + tr.n_flows / 32.0) * (2.0 if s.policy == _abi.POLICY_MQFQ else 1.0)
+                   * (1.0 + 1.0 / max(d, 1)))
+    return out
+
+
+def restrict(w: Workload, idx) -> Workload:
+    """The same workload (traces, tables, configs) with only sims ``idx``."""
+    idx = list(idx)
+    return Workload(w.name, w.traces, w.tabs, w.dcfgs, [w.sims[i] for i in idx], w.groups,
+                    w.hist_rows, dict(w.describe, sims=len(idx)))
+
+
 def build(name: str, rank: int = 0, engine=None, **kw) -> Workload:
     """Weak-scaling shard for `rank`: a disjoint block of seeds per GPU.
     With an engine the traces are generated on its GPU."""
+    if name in ("c1", "c1f10"):
+        return c1("f10" if name == "c1f10" else "default", engine=engine)
     if name == "c3":
         n = kw.get("n_seeds", 16)
         return c3(seed_base=1 + rank * n, n_seeds=n, engine=engine)

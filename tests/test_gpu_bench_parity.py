@@ -63,7 +63,7 @@ def _check(eng, w, n_sample, seed=0, flags=0, expect=None):
     assert int(bench[_abi.OUT_HIST].sum()) == int(n_arr.sum())
     # a random sample against the oracle (ctypes releases the GIL: threads)
     rng = np.random.default_rng(seed)
-    bad = []
+    bad, work = [], []
     sample = sorted(rng.choice(len(w.sims), n_sample, replace=False).tolist())
 
     def oracle_run(i):
@@ -73,7 +73,8 @@ def _check(eng, w, n_sample, seed=0, flags=0, expect=None):
         return orc.run_packed(_abi.Sim.from_buffer_copy(s), tr.arrival, tr.flow, tr.n_flows,
                               {"warm": tab.warm, "cold": tab.cold, "mem": tab.mem,
                                "share": tab.share, "weight": tab.weight},
-                              [_abi.device_cfg_from(d) for d in dc], want_audit=False)
+                              [_abi.device_cfg_from(d) for d in dc], want_audit=False,
+                              early_exit=True)
 
     with ThreadPoolExecutor(max_workers=16) as ex:
         refs = list(ex.map(oracle_run, sample))
@@ -97,7 +98,12 @@ def _check(eng, w, n_sample, seed=0, flags=0, expect=None):
               and res.summary[i, 2] == r["mean_util"])
         if not ok:
             bad.append(i)
+        # the same early exit in both (bench arms do identical work): the
+        # processed events and dispatch() calls agree too
+        if (int(c[i, 0]), int(c[i, 1])) != (r["n_events"], r["n_dispatch_calls"]):
+            work.append((i, int(c[i, 0]), r["n_events"], int(c[i, 1]), r["n_dispatch_calls"]))
     assert not bad, f"{len(bad)} of {n_sample} sampled sims differ from the oracle: {bad[:10]}"
+    assert not work, f"event / dispatch-call counts differ (sim, gpu, oracle): {work[:5]}"
 
 
 def test_c3_full_sweep(engine):
