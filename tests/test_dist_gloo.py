@@ -1,8 +1,10 @@
 """World-size-2 gloo run of the multi-GPU sweep plumbing on CPU: each rank
-takes its shard of a small sweep, simulates it with the CPU oracle (as the
-stand-in for its GPU), bins latencies into the sweep histogram and the
-ranks all-reduce; the result must equal the single-process histogram of the
-whole sweep, and the gathered summary rows must cover every simulation."""
+takes its part of a small fixed sweep (dist.partition, the strong split
+bench.py --split strong uses), simulates it with the CPU oracle (as the
+stand-in for its GPU; tests/test_gpu_dist.py runs the same with libgfq),
+bins latencies into the sweep histogram and the ranks all-reduce; the
+result must equal the single-process histogram of the whole sweep, and the
+gathered summary rows must cover every simulation."""
 
 from __future__ import annotations
 
@@ -26,12 +28,12 @@ def _free_port():
 def _shard_hist(rank, world):
     from oracle import oracle as orc
     from paper_2507_08954_b200 import _abi, sweep
-    from paper_2507_08954_b200.dist import hist_bin, shard_bounds
+    from paper_2507_08954_b200.dist import hist_bin, partition
     w = sweep.c3(n_seeds=1, duration=40.0)
-    lo, hi = shard_bounds(len(w.sims), rank, world)
+    part = partition(sweep.sim_costs(w), world)[rank]
     hist = np.zeros((w.groups, w.hist_rows, sweep.HIST_BINS), dtype=np.int64)
     rows = []
-    for i in range(lo, hi):
+    for i in part:
         s = w.sims[i]
         tr, tab = w.traces[s.trace], w.tabs[s.flowtab]
         r = orc.run_packed(_abi.Sim.from_buffer_copy(s), tr.arrival, tr.flow, tr.n_flows,
@@ -77,3 +79,17 @@ def test_two_rank_histogram_reduction():
     got = rows[rows[:, 0] >= 0]
     got = got[np.argsort(got[:, 0])]
     assert np.array_equal(got, ref_rows)
+
+
+def test_partition_is_a_balanced_cover():
+    from paper_2507_08954_b200 import sweep
+    from paper_2507_08954_b200.dist import partition
+    w = sweep.c5(n_traces=3, duration=60.0)
+    costs = sweep.sim_costs(w)
+    for world in (1, 2, 3, 8):
+        parts = partition(costs, world)
+        flat = sorted(i for p in parts for i in p)
+        assert flat == list(range(len(costs)))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+        loads = [sum(costs[i] for i in p) for p in parts]
+        assert max(loads) <= sum(costs) / world + max(costs)      # LPT bound
