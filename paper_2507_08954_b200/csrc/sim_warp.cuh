@@ -960,32 +960,6 @@ struct WarpSim {
         return effd;
     }
 
-    // The sample-ring half of monitor_tick (1-device build, device state in
-    // registers) for a fast-forwarded tick (see the tick run in run()): the
-    // new (now, util) sample, the horizon pops, the id shift register.  The
-    // window average / effective_d / headroom half is not recomputed: its
-    // registers keep the values of the last full tick together with that
-    // tick's memo key (LKEY), and a later full tick recomputes from the key,
-    // so a stale pair is never misread.
-    FI void window_push1(double util, int id) {
-        const int S = P.L.S;
-        int head = hv[DV_SHEAD], ns = hv[DV_SN];
-        int w = head + ns; if (w >= S) w -= S;
-        USYNC();
-        SMPT(0, w) = now; SMPU(0, w) = util;
-        double oldt = ns == 0 ? now : hd[DD_OLDT];
-        ns++;
-        const double horizon = now - win0;
-        #pragma unroll 1
-        while (ns > 0 && oldt <= horizon) {
-            head++; if (head >= S) head = 0; ns--;
-            oldt = SMPT(0, head);
-        }
-        hv[DV_SHEAD] = head; hv[DV_SN] = ns; hd[DD_OLDT] = oldt;
-        hv[DV_WCODE] = (int)(((uint32_t)hv[DV_WCODE] << 4) | (uint32_t)id);
-        hv[DV_ZAGE] = id ? min(hv[DV_ZAGE] + 1, 15) : 0;
-    }
-
     // ==================================================================
     // scheduler (mqfq.py) and baseline policies (policies.py)
 
@@ -1582,13 +1556,6 @@ struct WarpSim {
                 // effective_d / headroom flag move from tick to tick
                 const bool q_gvt = !MQFQ || gmin_ok;
                 const bool q_idle = tot_pend == 0, q_busy = tot_infl > 0;
-                // fast-forward eligibility (1-device builds, fixed D): the
-                // drain is quiet whatever the utilization window says --
-                // nothing pending, or every token out (out >= d_max ==
-                // effective_d) -- so a tick reduces to its sample, its
-                // mean-utilization term and its successor
-                const bool ff = !G && ND1 && q_gvt && !DV(0, DV_DYN) &&
-                                (q_idle | (q_busy & (hv[DV_OUT] >= DV(0, DV_DMAX))));
                 #pragma unroll 1
                 for (;;) {
                     tick_on = false;
@@ -1606,30 +1573,6 @@ struct WarpSim {
                     now = tick_t;
                     n_events++;
                     dr = true;
-                    if (ff) {
-                        // Fast-forward (exact): while this tick is quiet and the
-                        // one after it still belongs to the run, process it as
-                        // the full path would -- the running set is unchanged,
-                        // so its sample is the cached instantaneous_util; work
-                        // remains, so the next tick is pushed -- minus the
-                        // window-average half (window_push1).  The last tick
-                        // of the run goes through the full path above.
-                        const double u = hd[DD_INST];
-                        const int uid = hv[DV_INSTID];
-                        #pragma unroll 1
-                        while ((!MQFQ | (now < idle_lb)) & (now + period < lim) &
-                               (n_events < max_events)) {
-                            diag(DG_TICKS);
-                            if (u != 0.0) ps_add(util_sum, u);
-                            window_push1(u, uid);
-                            n_util++;
-                            push_tick(now + period);
-                            n_calls++;
-                            diag(DG_QUIET);
-                            now = tick_t;
-                            n_events++;
-                        }
-                    }
                 }
             } else {
                 int slot = pmin_slot;
