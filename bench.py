@@ -608,10 +608,18 @@ class _CudaArray:
 
 
 def e2e_run(eng, w, outputs, kw, steps, world, dist):
-    """Public-API end-to-end: host->device uploads from pinned buffers, one
-    launch, device->host results, every step (wall clock, max over ranks)."""
+    """Public-API end-to-end, every step: host->device uploads of the step's
+    traces / flow tables / configs / sim blocks from pinned buffers,
+    gfq_prepare, launch, and the device->host read of its results (status,
+    counters, summary, per-function statistics) into pinned buffers.  Wall
+    clock, max over ranks.  Two engine handles alternate (double buffering):
+    step k's uploads and step k-1's result reads run on each handle's
+    transfer stream while the other handle's kernel runs, so the host work
+    hides behind the simulation kernels; every step still moves all of its
+    bytes."""
     import torch
     from paper_2507_08954_b200 import _abi
+    from paper_2507_08954_b200.engine import Engine
 
     def pinned(a):
         t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
@@ -629,39 +637,47 @@ def e2e_run(eng, w, outputs, kw, steps, world, dist):
     h2d = (arrival.nbytes + flow.nbytes + toff.nbytes + tnf.nbytes + sum(c.nbytes for c in cols)
            + hrow.nbytes + tabo.nbytes + 88 * len(w.dcfgs) + 96 * len(w.sims))
     sims = w.sims_array()
+    engs = [eng, Engine(eng.device)]
+    stream = torch.cuda.Stream()                  # both handles' kernels, in order
 
-    # results land in pinned host buffers (full-bandwidth device->host reads)
     res_ids = (_abi.OUT_STATUS, _abi.OUT_COUNTERS, _abi.OUT_SUMMARY, _abi.OUT_FLOW_COUNT,
                _abi.OUT_FLOW_MEAN, _abi.OUT_FLOW_VAR, _abi.OUT_FLOW_COLD_PCT)
     eng.prepare(sims, outputs=outputs, early_exit=True, **kw)
-    res_buf = {oid: pinned(np.zeros(eng.output(oid).shape, dtype=eng.output(oid).dtype))
-               for oid in res_ids}
+    res_buf = [{oid: pinned(np.zeros(eng.output(oid).shape, dtype=eng.output(oid).dtype))
+                for oid in res_ids} for _ in engs]
 
-    def one():
-        eng.upload_trace_arrays(arrival, flow, toff, tnf)
-        eng.upload_flowtab_arrays(*cols, hrow, tabo)
-        eng.upload_device_cfgs(w.dcfgs)
-        eng.prepare(sims, outputs=outputs, early_exit=True, **kw)
-        eng.launch()
-        eng.synchronize()
+    def submit(e):
+        e.upload_trace_arrays(arrival, flow, toff, tnf)
+        e.upload_flowtab_arrays(*cols, hrow, tabo)
+        e.upload_device_cfgs(w.dcfgs)
+        e.prepare(sims, outputs=outputs, early_exit=True, **kw)
+        e.launch(stream)
+
+    def collect(k):
+        e, buf = engs[k % 2], res_buf[k % 2]
+        e.synchronize()
         n = 0
         for oid in res_ids:
-            n += eng.output_into(oid, res_buf[oid]).nbytes
-        c = res_buf[_abi.OUT_COUNTERS].reshape(-1, _abi.NCOUNTERS)
+            n += e.output_into(oid, buf[oid]).nbytes
+        c = buf[_abi.OUT_COUNTERS].reshape(-1, _abi.NCOUNTERS)
         return int(c[:, 2].sum()), n
 
-    one()
+    for k in range(2):                            # warm both handles
+        submit(engs[k]); collect(k)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    disp = 0
-    got = 0
-    for _ in range(steps):
-        d, got = one()
-        disp += d
-    torch.cuda.synchronize()
+    disp = got = 0
+    for k in range(steps):
+        submit(engs[k % 2])
+        if k:
+            d, got = collect(k - 1)
+            disp += d
+    d, got = collect(steps - 1)
+    disp += d
     dt = time.perf_counter() - t0
+    engs[1].close()
     if dist:
         t = torch.tensor([dt, float(disp)], dtype=torch.float64,
                          device="cuda" if dist.get_backend() == "nccl" else "cpu")
@@ -670,7 +686,9 @@ def e2e_run(eng, w, outputs, kw, steps, world, dist):
         dt, disp = float(tm.item()), float(td.item())
     return {"value": disp / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(got), "steps": steps,
-            "ms_per_step": 1e3 * dt / steps}
+            "ms_per_step": 1e3 * dt / steps,
+            "pipeline": "2 engine handles, double-buffered: step k's uploads + prepare and "
+                        "step k-1's result reads overlap the kernels"}
 
 
 def main():

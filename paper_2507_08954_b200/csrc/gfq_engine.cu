@@ -646,6 +646,11 @@ struct gfq_handle {
     std::vector<cudaEvent_t> ring;          // GFQ_TIMING_RING x 3 events
     int ring_next = 0, ring_count = 0;
     cudaStream_t last_stream = nullptr;
+    // host<->device copies of the per-batch API calls: a non-blocking stream,
+    // ordered after this handle's last launch (ev[2]) and synchronised before
+    // each call returns, so a call on one handle overlaps kernels of another
+    // (the e2e pipeline double-buffers two handles)
+    cudaStream_t xfer = nullptr;
     bool launched = false;
 };
 
@@ -687,6 +692,7 @@ int gfq_create(int device, gfq_handle** out) {
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     h->ring.resize(3 * GFQ_TIMING_RING);
     for (auto& e : h->ring) CK(cudaEventCreate(&e));
+    CK(cudaStreamCreateWithFlags(&h->xfer, cudaStreamNonBlocking));
     *out = h;
     return GFQ_OK;
 }
@@ -705,6 +711,7 @@ int gfq_destroy(gfq_handle* h) {
     for (auto& e : h->join) if (e) cudaEventDestroy(e);
     if (h->fork) cudaEventDestroy(h->fork);
     for (auto& q : h->side) if (q) cudaStreamDestroy(q);
+    if (h->xfer) cudaStreamDestroy(h->xfer);
     delete h;
     return GFQ_OK;
 }
@@ -717,6 +724,7 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
     if (!h || n_traces < 0 || (n_traces > 0 && (!off || !n_flows)))
         return set_err(GFQ_EINVAL, "gfq_upload_traces: bad arguments");
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamWaitEvent(h->xfer, h->ev[2], 0));      // after this handle's last launch
     if (off[0] != 0) return set_err(GFQ_EINVAL, "gfq_upload_traces: off[0] must be 0");
     int64_t total = n_traces ? off[n_traces] : 0;
     int32_t max_nf = 1;
@@ -740,22 +748,23 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
         (rc = h->foff_off.ensure(8 * (n_traces + 1))) || (rc = h->foff.ensure(4 * foff_off[n_traces])))
         return rc;
     if (total) {
-        CK(cudaMemcpy(h->arrival.p, arrival, 8 * total, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->flow.p, flow, 4 * total, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(h->arrival.p, arrival, 8 * total, cudaMemcpyHostToDevice, h->xfer));
+        CK(cudaMemcpyAsync(h->flow.p, flow, 4 * total, cudaMemcpyHostToDevice, h->xfer));
     }
-    CK(cudaMemcpy(h->trace_off.p, off, 8 * (n_traces + 1), cudaMemcpyHostToDevice));
-    if (n_traces) CK(cudaMemcpy(h->trace_nf.p, n_flows, 4 * n_traces, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(h->trace_off.p, off, 8 * (n_traces + 1), cudaMemcpyHostToDevice, h->xfer));
+    if (n_traces) CK(cudaMemcpyAsync(h->trace_nf.p, n_flows, 4 * n_traces, cudaMemcpyHostToDevice, h->xfer));
     // per-arrival validation (engine.py:50-52,72-73) on the GPU; the first
     // failure in (trace, position, check) order is the one reported, as a
     // sequential scan would.  On failure no traces stay resident.
     if (total) {
         if ((rc = h->verr.ensure(8))) return rc;
-        CK(cudaMemset(h->verr.p, 0xff, 8));
-        k_validate_traces<<<n_traces, 256>>>(h->arrival.as<double>(), h->flow.as<int32_t>(), h->trace_off.as<int64_t>(),
+        CK(cudaMemsetAsync(h->verr.p, 0xff, 8, h->xfer));
+        k_validate_traces<<<n_traces, 256, 0, h->xfer>>>(h->arrival.as<double>(), h->flow.as<int32_t>(), h->trace_off.as<int64_t>(),
                                              h->trace_nf.as<int32_t>(), h->verr.as<unsigned long long>());
         CK(cudaGetLastError());
         unsigned long long e = 0;
-        CK(cudaMemcpy(&e, h->verr.p, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(&e, h->verr.p, 8, cudaMemcpyDeviceToHost, h->xfer));
+        CK(cudaStreamSynchronize(h->xfer));
         if (e != ~0ull) {
             const int t = (int)(e >> 29), kind = (int)(e & 3);
             h->n_traces = 0; h->h_trace_off.assign(1, 0); h->h_trace_nf.clear(); h->prepared = false;
@@ -771,16 +780,16 @@ int gfq_upload_traces(gfq_handle* h, const double* arrival, const int32_t* flow,
 // host-side trace table; arrival / flow / trace_off / trace_nf are on the device.
 static int index_traces(gfq_handle* h, const int64_t* off, const int32_t* n_flows, int32_t n_traces,
                         const std::vector<int64_t>& foff_off, int32_t max_nf) {
-    CK(cudaMemcpy(h->foff_off.p, foff_off.data(), 8 * (n_traces + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(h->foff_off.p, foff_off.data(), 8 * (n_traces + 1), cudaMemcpyHostToDevice, h->xfer));
     if (n_traces) {
         size_t sm = 4 * ((size_t)max_nf + 1);
         if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_trace_index, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_trace_index<<<n_traces, 32, sm>>>(h->flow.as<int32_t>(), h->trace_off.as<int64_t>(),
+        k_trace_index<<<n_traces, 32, sm, h->xfer>>>(h->flow.as<int32_t>(), h->trace_off.as<int64_t>(),
                                             h->trace_nf.as<int32_t>(), h->foff_off.as<int64_t>(),
                                             h->foff.as<int32_t>(), h->fpos.as<int32_t>(), n_traces);
         CK(cudaGetLastError());
-        CK(cudaDeviceSynchronize());
     }
+    CK(cudaStreamSynchronize(h->xfer));
     h->h_trace_off.assign(off, off + n_traces + 1);
     h->h_trace_nf.assign(n_flows, n_flows + n_traces);
     h->n_traces = n_traces;
@@ -794,6 +803,7 @@ int gfq_generate_traces(gfq_handle* h, int32_t n_traces, const int32_t* n_functi
     if (!h || n_traces < 0 || (n_traces > 0 && (!n_functions || !rates || !name_rank || !duration_s || !seed)))
         return set_err(GFQ_EINVAL, "gfq_generate_traces: bad arguments");
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamWaitEvent(0, h->ev[2], 0));   // legacy-stream work after this handle's last launch
     // streams of a trace in name order: stream (t, j) is the function whose
     // name rank is j, so a stable sort by time gives (t, name) order
     std::vector<int64_t> fn_off(n_traces + 1, 0);
@@ -912,6 +922,7 @@ int gfq_download_traces(gfq_handle* h, double* arrival, int32_t* flow, int64_t t
     const int64_t have = h->h_trace_off.empty() ? 0 : h->h_trace_off.back();
     if (total != have) return set_err(GFQ_EINVAL, "gfq_download_traces: total does not match the resident traces");
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamWaitEvent(0, h->ev[2], 0));   // legacy-stream work after this handle's last launch
     if (total && arrival) CK(cudaMemcpy(arrival, h->arrival.p, 8 * total, cudaMemcpyDeviceToHost));
     if (total && flow) CK(cudaMemcpy(flow, h->flow.p, 4 * total, cudaMemcpyDeviceToHost));
     return GFQ_OK;
@@ -932,6 +943,7 @@ int gfq_upload_flowtabs(gfq_handle* h, const double* warm_s, const double* cold_
         if (!(compute_share[i] > 0 && compute_share[i] <= 1)) return set_err(GFQ_EINVAL, "compute_share must be in (0, 1]");
         if (!(weight[i] > 0)) return set_err(GFQ_EINVAL, "weight must be > 0");
     }
+    CK(cudaStreamWaitEvent(h->xfer, h->ev[2], 0));      // after this handle's last launch
     int rc;
     if ((rc = h->warm.ensure(8 * total)) || (rc = h->cold.ensure(8 * total)) ||
         (rc = h->mem.ensure(8 * total)) || (rc = h->share.ensure(8 * total)) ||
@@ -939,15 +951,16 @@ int gfq_upload_flowtabs(gfq_handle* h, const double* warm_s, const double* cold_
         (rc = h->tab_off.ensure(8 * (n_tabs + 1))))
         return rc;
     if (total) {
-        CK(cudaMemcpy(h->warm.p, warm_s, 8 * total, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->cold.p, cold_s, 8 * total, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->mem.p, mem_mb, 8 * total, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->share.p, compute_share, 8 * total, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->weight.p, weight, 8 * total, cudaMemcpyHostToDevice));
-        if (hist_row) CK(cudaMemcpy(h->hist_row.p, hist_row, 4 * total, cudaMemcpyHostToDevice));
-        else CK(cudaMemset(h->hist_row.p, 0, 4 * total));
+        CK(cudaMemcpyAsync(h->warm.p, warm_s, 8 * total, cudaMemcpyHostToDevice, h->xfer));
+        CK(cudaMemcpyAsync(h->cold.p, cold_s, 8 * total, cudaMemcpyHostToDevice, h->xfer));
+        CK(cudaMemcpyAsync(h->mem.p, mem_mb, 8 * total, cudaMemcpyHostToDevice, h->xfer));
+        CK(cudaMemcpyAsync(h->share.p, compute_share, 8 * total, cudaMemcpyHostToDevice, h->xfer));
+        CK(cudaMemcpyAsync(h->weight.p, weight, 8 * total, cudaMemcpyHostToDevice, h->xfer));
+        if (hist_row) CK(cudaMemcpyAsync(h->hist_row.p, hist_row, 4 * total, cudaMemcpyHostToDevice, h->xfer));
+        else CK(cudaMemsetAsync(h->hist_row.p, 0, 4 * total, h->xfer));
     }
-    CK(cudaMemcpy(h->tab_off.p, off, 8 * (n_tabs + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(h->tab_off.p, off, 8 * (n_tabs + 1), cudaMemcpyHostToDevice, h->xfer));
+    CK(cudaStreamSynchronize(h->xfer));
     h->h_tab_off.assign(off, off + n_tabs + 1);
     h->h_mem.assign(mem_mb, mem_mb + total);
     h->n_tabs = n_tabs;
@@ -967,9 +980,11 @@ int gfq_upload_device_cfgs(gfq_handle* h, const gfq_device_cfg* cfgs, int32_t n)
         if (!(c.interference_beta >= 0)) return set_err(GFQ_EINVAL, "interference_beta must be >= 0");
     }
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamWaitEvent(h->xfer, h->ev[2], 0));
     int rc = h->dcfg.ensure(sizeof(gfq_device_cfg) * std::max(n, 1));
     if (rc) return rc;
-    if (n) CK(cudaMemcpy(h->dcfg.p, cfgs, sizeof(gfq_device_cfg) * n, cudaMemcpyHostToDevice));
+    if (n) CK(cudaMemcpyAsync(h->dcfg.p, cfgs, sizeof(gfq_device_cfg) * n, cudaMemcpyHostToDevice, h->xfer));
+    CK(cudaStreamSynchronize(h->xfer));
     h->h_dcfg.assign(cfgs, cfgs + n);
     h->prepared = false;
     return GFQ_OK;
@@ -978,9 +993,11 @@ int gfq_upload_device_cfgs(gfq_handle* h, const gfq_device_cfg* cfgs, int32_t n)
 int gfq_upload_execs(gfq_handle* h, const double* execs, int64_t n) {
     if (!h || n < 0 || (n > 0 && !execs)) return set_err(GFQ_EINVAL, "gfq_upload_execs: bad arguments");
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamWaitEvent(h->xfer, h->ev[2], 0));
     int rc = h->execs.ensure(8 * std::max<int64_t>(n, 1));
     if (rc) return rc;
-    if (n) CK(cudaMemcpy(h->execs.p, execs, 8 * n, cudaMemcpyHostToDevice));
+    if (n) CK(cudaMemcpyAsync(h->execs.p, execs, 8 * n, cudaMemcpyHostToDevice, h->xfer));
+    CK(cudaStreamSynchronize(h->xfer));
     h->n_execs = n;
     h->prepared = false;
     return GFQ_OK;
@@ -1276,12 +1293,14 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     for (int i = 0; i < n_sims; i++) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
         return cls[a] != cls[b] ? cls[a] < cls[b] : cost[a] > cost[b]; });
+    CK(cudaStreamWaitEvent(h->xfer, h->ev[2], 0));      // after this handle's last launch
     if (n_sims) {
-        CK(cudaMemcpy(h->sims.p, sims, sizeof(gfq_sim) * n_sims, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->order.p, order.data(), 4 * n_sims, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(h->sims.p, sims, sizeof(gfq_sim) * n_sims, cudaMemcpyHostToDevice, h->xfer));
+        CK(cudaMemcpyAsync(h->order.p, order.data(), 4 * n_sims, cudaMemcpyHostToDevice, h->xfer));
     }
-    CK(cudaMemcpy(h->sim_foff.p, foffs.data(), 8 * (n_sims + 1), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->sim_roff.p, roffs.data(), 8 * (n_sims + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(h->sim_foff.p, foffs.data(), 8 * (n_sims + 1), cudaMemcpyHostToDevice, h->xfer));
+    CK(cudaMemcpyAsync(h->sim_roff.p, roffs.data(), 8 * (n_sims + 1), cudaMemcpyHostToDevice, h->xfer));
+    CK(cudaStreamSynchronize(h->xfer));
     h->h_sims.assign(sims, sims + n_sims);
     h->h_sim_foff = foffs; h->h_sim_roff = roffs;
     h->n_sims = n_sims;
@@ -1440,7 +1459,8 @@ int gfq_synchronize(gfq_handle* h) {
     CK(cudaEventSynchronize(h->ev[2]));
     if (h->n_sims == 0) return GFQ_OK;
     std::vector<int32_t> st(h->n_sims);
-    CK(cudaMemcpy(st.data(), h->out[GFQ_OUT_STATUS].p, 4 * h->n_sims, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(st.data(), h->out[GFQ_OUT_STATUS].p, 4 * h->n_sims, cudaMemcpyDeviceToHost, h->xfer));
+    CK(cudaStreamSynchronize(h->xfer));
     for (int i = 0; i < h->n_sims; i++)
         if (st[i] != GFQ_SIM_OK) {
             static const char* names[] = {"ok", "dynamic event pool overflow", "utilization-sample buffer overflow",
@@ -1596,7 +1616,11 @@ int gfq_output_copy(gfq_handle* h, int32_t id, void* host_dst, int64_t bytes) {
     int64_t have = h->out_n[id] * kOutBytes[id];
     if (bytes > have) return set_err(GFQ_EINVAL, "gfq_output_copy: request larger than the output");
     CK(cudaSetDevice(h->device));
-    if (bytes) CK(cudaMemcpy(host_dst, h->out[id].p, bytes, cudaMemcpyDeviceToHost));
+    if (bytes) {
+        CK(cudaStreamWaitEvent(h->xfer, h->ev[2], 0));  // after this handle's last launch
+        CK(cudaMemcpyAsync(host_dst, h->out[id].p, bytes, cudaMemcpyDeviceToHost, h->xfer));
+        CK(cudaStreamSynchronize(h->xfer));
+    }
     return GFQ_OK;
 }
 
@@ -1621,6 +1645,7 @@ int gfq_fairness(gfq_handle* h, double window_s, const int32_t* d_max,
     for (int64_t i = 0; i < n_weights; i++)
         if (!(report_weight[i] > 0)) return set_err(GFQ_EINVAL, "weights must be positive");
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamWaitEvent(0, h->ev[2], 0));   // legacy-stream work after this handle's last launch
     CK(cudaEventSynchronize(h->ev[2]));
     const int n = h->n_sims;
     std::vector<double> ft(std::max(n, 1));
