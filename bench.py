@@ -71,6 +71,10 @@ def parse():
     ap.add_argument("--impl", default="gfq", choices=["gfq", "reference"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c1", "c1f10", "c2", "c4", "c5"])
     ap.add_argument("--split", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="--split strong on ONE GPU: run the part of rank --emulate-rank of a "
+                         "sweep split over this many ranks (per-rank time of an N-GPU run)")
+    ap.add_argument("--emulate-rank", type=int, default=0)
     ap.add_argument("--py-seconds", type=float, default=15.0,
                     help="wall seconds of the unmodified Python reference sample (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -331,6 +335,44 @@ def source_hash() -> str:
     return h.hexdigest()[:12]
 
 
+def _norm_kernel(name: str) -> str:
+    import re
+    name = re.sub(r"\bgfq::", "", name).replace("true", "1").replace("false", "0")
+    return name.replace(" ", "")
+
+
+def kernel_sass_hashes(so=None) -> dict:
+    """sha256 of each simulation kernel's SASS in libgfq.so, by normalised
+    demangled name: ties an ncu capture to the exact machine code measured
+    (host-side edits to the engine do not invalidate it)."""
+    import hashlib
+    import re
+    so = so or os.path.join(ROOT, "paper_2507_08954_b200", "libgfq.so")
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True,
+                             timeout=120).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        return {}
+    funcs, cur, buf = {}, None, []
+    for ln in out.splitlines():
+        m = re.search(r"Function : (\S+)", ln)
+        if m:
+            if cur:
+                funcs[cur] = "\n".join(buf)
+            cur, buf = m.group(1), []
+        elif cur:
+            buf.append(ln)
+    if cur:
+        funcs[cur] = "\n".join(buf)
+    names = [k for k in funcs if "k_sim" in k]
+    if not names:
+        return {}
+    dem = subprocess.run(["c++filt"], input="\n".join(names), capture_output=True,
+                         text=True).stdout.splitlines()
+    return {_norm_kernel(d): hashlib.sha256(funcs[m].encode()).hexdigest()[:16]
+            for m, d in zip(names, dem)}
+
+
 def ncu_capture(workload: str):
     """The committed ncu --set full numbers of this workload's dominant
     kernel (tools/ncu_summary.py -> profiles/ncu_k_sim_<workload>.json)."""
@@ -369,8 +411,12 @@ def run_gfq(args):
         from paper_2507_08954_b200.dist import partition
         w_full = sweep.build(args.workload, 0, engine=eng,
                              **({"n_seeds": args.seeds} if args.seeds else {}))
-        part = partition(sweep.sim_costs(w_full), world)[rank]
+        ew = args.emulate_world or world
+        er = args.emulate_rank if args.emulate_world else rank
+        part = partition(sweep.sim_costs(w_full), ew)[er]
         w = sweep.restrict(w_full, part)
+        w.describe["strong_part"] = {"ranks": ew, "rank": er, "sims": len(part),
+                                     "emulated_on_one_gpu": bool(args.emulate_world)}
     else:
         w = sweep.build(args.workload, rank, engine=eng,
                         **({"n_seeds": args.seeds} if args.seeds else {}))
@@ -529,7 +575,9 @@ def rooflines(w, workload, kern_ms, disp, events, calls, clocks, info):
     mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
     peak_issue = n_sm * 4 * mhz * 1e6 / 1e9          # G warp-instructions / s
     inst = nc.get("inst_executed_per_launch")
-    same = nc.get("source_hash") == source_hash() and nc.get("sims") == len(w.sims)
+    kern = _norm_kernel(nc.get("kernel", ""))
+    same = bool(nc) and nc.get("kernel_sass_hash") == kernel_sass_hashes().get(kern) \
+        and nc.get("sims") == len(w.sims)
     roof = {"bound": "sm_issue", "unit": "G warp-inst/s", "peak": peak_issue,
             "peak_source": f"{n_sm} SMs x 4 issue slots x {mhz:.0f} MHz (sampled SM clock)",
             "achieved": None, "frac": None, "traffic": nc.get("dram_bytes_per_launch"),

@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from bench import source_hash  # noqa: E402
+from bench import _norm_kernel, kernel_sass_hashes, source_hash  # noqa: E402
 
 rep, name, workload, sims = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
 algo_bytes = float(sys.argv[5]) if len(sys.argv) > 5 else 0
@@ -59,6 +59,7 @@ if algo_bytes:
 open(f"profiles/{name}.txt", "w").write("\n".join(out) + "\n")
 json.dump({"capture": f"profiles/{name}.txt", "workload": workload, "sims": sims,
            "kernel": d["Kernel Name"][0], "source_hash": source_hash(),
+           "kernel_sass_hash": kernel_sass_hashes().get(_norm_kernel(d["Kernel Name"][0])),
            "inst_executed_per_launch": inst, "cycles_elapsed": cyc,
            "duration_ms": float(d["gpu__time_duration.sum"][0]),
            "issue_frac_elapsed": inst / (cyc * n_sm * 4),
