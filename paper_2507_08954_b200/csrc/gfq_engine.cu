@@ -348,6 +348,7 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA, FG>& w, const Par
     w.n_events = 0;
     w.n_calls = w.n_disp = w.n_comp = w.n_util = w.n_backlog = w.n_evlog = 0;
     w.n_evict = 0;
+    w.nbl = 0;
     ps_init(w.util_sum);
 
     // Simulation.__init__, engine.py:70-78: arrivals own seq 0..n-1, the first

@@ -46,7 +46,7 @@ enum { CTA_MAXW = 32 };
 #endif
 struct CtaCmd {
     int32_t op, nf, nev, iarg;     // scan kind, flow count, event slots, use_inf
-    int32_t newly_n, flag, pad0, pad1;
+    int32_t newly_n, flag, nset, pad1;     // nset: backlogged-set size (large-flow builds)
     double gvt, now;
     unsigned long long pk[CTA_MAXW];
     uint32_t ps[CTA_MAXW];
@@ -87,6 +87,10 @@ struct Layout {
     // warp 0 runs the event loop, the other warps join its O(F) scans
     int32_t cta;
     int32_t bytes;                                       // shared bytes per warp (per CTA in CTA mode)
+    // large-flow builds (CTA or flows in global): the set of backlogged flows
+    // (pending or in flight) as an unordered list + position index, so the
+    // global-VT and candidate scans visit backlogged flows only
+    int32_t o_bll, o_blp;                                // u16[F], u16[F] (fe part; 0 = none)
 };
 
 struct Params {
@@ -150,6 +154,8 @@ inline void layout_finish(Layout& L) {
     L.o_fst = take(F);
     L.o_ev_t = take(8 * E); L.o_ev_seq = take(4 * E); L.o_ev_meta = take(4 * E);
     L.o_cnt = take(2 * 3 * ND * F);
+    if (L.cta || L.flows_global) { L.o_bll = take(2 * F); L.o_blp = take(2 * F); }
+    else L.o_bll = L.o_blp = 0;
     L.fe_bytes = o;
     o = 0;
     auto take16 = [&](int32_t bytes) { o = (o + 15) & ~15; return take(bytes); };

@@ -211,6 +211,10 @@ struct WarpSim {
     static constexpr int SCAN_UNROLL = FG ? GFQ_FG_UNROLL : 1;
     static constexpr bool RING = CTA && GFQ_RING;
     static constexpr bool CSTAGE = CTA && GFQ_CSTAGE;
+    // large-flow builds: the global-VT / candidate scans visit the set of
+    // backlogged flows (pending or in flight: at most the queued invocations
+    // plus the tokens out) instead of every touched flow
+    static constexpr bool SETS = CTA || FG;
     const Params& P;
     unsigned char* const sm;   // device part of this warp's state (shared memory)
     unsigned char* const fe;   // flow/event part (shared memory, or global scratch)
@@ -230,6 +234,8 @@ struct WarpSim {
     FI int* done() const { return (int*)(fe + P.L.o_done); }
     FI int* pend() const { return (int*)(fe + P.L.o_pend); }
     FI uint8_t* fst() const { return (uint8_t*)(fe + P.L.o_fst); }
+    FI uint16_t* BLL() const { return (uint16_t*)(fe + P.L.o_bll); }   // backlogged set (SETS)
+    FI uint16_t* BLP() const { return (uint16_t*)(fe + P.L.o_blp); }   // flow -> its slot
     FI double* ev_t() const { return (double*)(fe + P.L.o_ev_t); }
     FI uint32_t* ev_seq() const { return (uint32_t*)(fe + P.L.o_ev_seq); }
     FI uint32_t* ev_meta() const { return (uint32_t*)(fe + P.L.o_ev_meta); }
@@ -383,6 +389,7 @@ struct WarpSim {
     double idle_lb;                    // (B) no keep-alive can expire before this
     int n_events;
     int n_calls, n_disp, n_comp, n_util, n_backlog, n_evlog;
+    int nbl;                           // SETS: backlogged-set size
     int n_evict;                       // Device.eviction_log rows (generic build)
     PySum util_sum;
 
@@ -399,11 +406,12 @@ struct WarpSim {
     // f = wid*32 + lane + k*nthr), reduced over the warp.
     FI Arg cta_part(int op) {
         Arg a = arg_none();
-        const int lim = op == OP_EVMIN ? nev : nf;
+        const bool set_op = SETS && op != OP_EVMIN && op != OP_REFRESH;
+        const int lim = op == OP_EVMIN ? nev : set_op ? nbl : nf;
         #pragma unroll 1
         for (int b = wid * 32; b < lim; b += nthr) {
-            const int f = b + lane;
-            const bool in = f < lim;
+            const bool in = b + lane < lim;
+            const int f = set_op ? (in ? (int)BLL()[b + lane] : 0) : b + lane;
             if (op == OP_GVT) {
                 if (in && pt()[f] - done()[f] > 0) { u64 k = okey(vt()[f]); if (k < a.k) a.k = k; }
             } else if (op == OP_CAND) {
@@ -420,7 +428,7 @@ struct WarpSim {
             } else if (op == OP_SJF) {
                 if (in && pend()[f] > 0) {
                     u64 k = okey(tau()[f]);
-                    if (k < a.k) { a.k = k; a.i = f; }
+                    if (k < a.k || (k == a.k && f < a.i)) { a.k = k; a.i = f; }
                 }
             } else if (op == OP_EVMIN) {
                 if (in) {
@@ -463,7 +471,7 @@ struct WarpSim {
         CtaCmd* c = cmd();
         __syncwarp();
         if (lane == 0) {
-            c->op = op; c->nf = nf; c->nev = nev; c->iarg = use_inf_;
+            c->op = op; c->nf = nf; c->nev = nev; c->iarg = use_inf_; c->nset = nbl;
             c->gvt = gvt; c->now = now;
         }
         cta_bar(1, nthr);
@@ -483,7 +491,7 @@ struct WarpSim {
             cta_bar(1, nthr);
             const int op = c->op;
             if (op == OP_EXIT) break;
-            nf = c->nf; nev = c->nev; use_inf_ = c->iarg; gvt = c->gvt; now = c->now;
+            nf = c->nf; nev = c->nev; use_inf_ = c->iarg; gvt = c->gvt; now = c->now; nbl = c->nset;
             Arg a = cta_part(op);
             if (lane == 0) { c->pk[wid] = a.k; c->ps[wid] = a.s; c->pi[wid] = a.i; }
             cta_bar(2, nthr);
@@ -556,6 +564,25 @@ struct WarpSim {
         }
         pmin_ok = false;
     }
+
+    // Backlogged set (SETS builds): unordered list + position index.  A flow
+    // enters when its backlog (arrived - completed) leaves 0 and leaves when it
+    // returns to 0; every scan over it reduces order-independently (min keys
+    // that end in the flow id), so results equal the full scans'.
+    FI void bl_add(int f) {
+        USYNC();
+        BLL()[nbl] = (uint16_t)f; BLP()[f] = (uint16_t)nbl;
+        nbl++;
+    }
+    FI void bl_remove(int f) {
+        const int p = BLP()[f];
+        const int last = BLL()[nbl - 1];
+        USYNC();
+        BLL()[p] = (uint16_t)last; BLP()[last] = (uint16_t)p;
+        nbl--;
+    }
+    FI int scan_n() const { return SETS ? nbl : nf; }                 // flows a set scan visits
+    FI int scan_f(int i) const { return SETS ? (int)BLL()[i] : i; }   // i-th of them
 
     // ==================================================================
     // device model (device.py)
@@ -966,7 +993,7 @@ struct WarpSim {
     // (A) recompute_global_vt, mqfq.py:114-127.  INACTIVE => not backlogged,
     // so the filter is "backlogged"; the minimum is cached (gmin).
     FI void recompute_gvt() {
-        if (!gmin_ok && cta_on(nf)) {
+        if (!gmin_ok && cta_on(scan_n())) {
             diag(DG_GSCAN);
             gmin = cta_scan(OP_GVT).k;
             gmin_ok = true;
@@ -974,9 +1001,12 @@ struct WarpSim {
         if (UNLIKELY(!gmin_ok)) {
             diag(DG_GSCAN);
             u64 bk = ~0ull;
+            const int ns = scan_n();
             #pragma unroll SCAN_UNROLL
-            for (int f = lane; f < nf; f += 32)
-                if (pt()[f] - done()[f] > 0) { u64 k = okey(vt()[f]); if (k < bk) bk = k; }
+            for (int i = lane; i < ns; i += 32) {
+                const int f = scan_f(i);
+                if (SETS || pt()[f] - done()[f] > 0) { u64 k = okey(vt()[f]); if (k < bk) bk = k; }
+            }
             gmin = wmin64(bk);
             gmin_ok = true;
         }
@@ -1048,14 +1078,16 @@ struct WarpSim {
     FI int mqfq_candidate() {
         diag(DG_CSCAN);
         bool use_inf = max_effective_d() != 1;
-        if (cta_on(nf)) {
+        if (cta_on(scan_n())) {
             use_inf_ = use_inf;
             u64 m = cta_scan(OP_CAND).k;
             return m == ~0ull ? -1 : (int)(m & 0xffffu);
         }
         u64 bk = ~0ull;
+        const int ns = scan_n();
         #pragma unroll SCAN_UNROLL
-        for (int f = lane; f < nf; f += 32) {
+        for (int i = lane; i < ns; i += 32) {
+            const int f = scan_f(i);
             int pe = pend()[f];
             if (pe > 0 && vt()[f] - gvt <= T) {
                 unsigned inf = use_inf ? (unsigned)infl()[f] : 0u;
@@ -1074,14 +1106,17 @@ struct WarpSim {
         if (dr >= 0 && (pend()[dr] > 0 || infl()[dr] > 0))
             return pend()[dr] == 0 ? -1 : dr;                // hold for late arrivals
         diag(DG_CSCAN);
-        if (cta_on(nf)) {
+        if (cta_on(scan_n())) {
             u64 m = cta_scan(OP_BATCH).k;
             return m == ~0ull ? -1 : flw((int)m);
         }
         unsigned bk = 0xffffffffu;
+        const int ns = scan_n();
         #pragma unroll SCAN_UNROLL
-        for (int f = lane; f < nf; f += 32)
+        for (int i = lane; i < ns; i += 32) {
+            const int f = scan_f(i);
             if (pend()[f] > 0) bk = min(bk, (unsigned)head()[f]);
+        }
         unsigned m = wmin32(bk);
         return m == 0xffffffffu ? -1 : flw((int)m);
     }
@@ -1089,14 +1124,20 @@ struct WarpSim {
     // SjfPolicy.dispatch, policies.py:245-262: min tau.mean, name order on ties
     FI int sjf_candidate() {
         diag(DG_CSCAN);
-        if (cta_on(nf)) {
+        if (cta_on(scan_n())) {
             Arg a = cta_scan(OP_SJF);
             return a.k == ~0ull ? -1 : a.i;
         }
         u64 bk = ~0ull; int bf = 0x7fffffff;
+        const int ns = scan_n();
         #pragma unroll SCAN_UNROLL
-        for (int f = lane; f < nf; f += 32)
-            if (pend()[f] > 0) { u64 k = okey(tau()[f]); if (k < bk) { bk = k; bf = f; } }
+        for (int i = lane; i < ns; i += 32) {
+            const int f = scan_f(i);
+            if (pend()[f] > 0) {
+                u64 k = okey(tau()[f]);
+                if (k < bk || (SETS && k == bk && f < bf)) { bk = k; bf = f; }   // name order on ties
+            }
+        }
         u64 m = wmin64(bk);
         if (m == ~0ull) return -1;
         return (int)wmin32(bk == m ? (unsigned)bf : 0x7fffffffu);
@@ -1373,6 +1414,7 @@ struct WarpSim {
     }
 
     FI void on_arrival(int inv, int fn) {                 // engine.py:121-129
+        if (SETS && pt()[fn] - done()[fn] == 0) bl_add(fn);            // backlog 0 -> 1
         if (!SCRIPTED) {
             if (pt()[fn] - done()[fn] == 0) backlog_audit(fn, true);   // _backlog_change(+1)
             if (UNLIKELY(fst()[fn] & FL_MARKED)) {         // unmark_evictable on every device
@@ -1434,6 +1476,7 @@ struct WarpSim {
         }
         __syncwarp();
         if (CSTAGE && (k & 31) == 31) comp_flush(32);
+        if (SETS && pt()[fn] - done()[fn] == 0) bl_remove(fn);         // backlog 1 -> 0
         if (!SCRIPTED && pt()[fn] - done()[fn] == 0) {     // _backlog_change(-1)
             backlog_audit(fn, false);
             if (MQFQ) push(now + ttl(fn), EV_EXPIRY, (uint32_t)fn);
