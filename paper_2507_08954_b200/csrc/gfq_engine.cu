@@ -367,6 +367,10 @@ __device__ __forceinline__ void sim_run(WarpSim<POL, ND1, CTA, FG>& w, const Par
         c[C_MAXEV] = dg[DG_MAXEV]; c[C_GSCAN] = dg[DG_GSCAN]; c[C_RSCAN] = dg[DG_RSCAN];
         c[C_CSCAN] = dg[DG_CSCAN]; c[C_TICKS] = dg[DG_TICKS]; c[C_WHIT] = dg[DG_WHIT];
         c[C_WMISS] = dg[DG_WMISS]; c[C_QUIET] = dg[DG_QUIET];
+#if GFQ_PROF
+        // -DGFQ_PROF=1 diagnostic build: cycles per phase (PF_*) in counters 5..11
+        for (int k = 0; k < 7; k++) c[C_GSCAN + k] = dg[DG_P0 + k];
+#endif
 #if GFQ_TIMELINE
         // -DGFQ_TIMELINE=1 diagnostic build: start / end (ns) and SM of each simulation
         unsigned long long tl1; unsigned smid;

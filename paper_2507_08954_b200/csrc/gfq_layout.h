@@ -33,7 +33,14 @@ enum { WDICT = 15, WMEMO = 64, WMEMO_BITS = 6, WMAXN = 7 };
 // flows queued for swap-out since the last _swap_out_inactive
 enum { NEWLY_CAP = 32 };
 // per-warp diagnostic counters (shared memory, lane 0 increments)
-enum { DG_MAXEV = 0, DG_GSCAN, DG_RSCAN, DG_CSCAN, DG_TICKS, DG_WHIT, DG_WMISS, DG_QUIET, DG_N };
+#ifndef GFQ_PROF
+#define GFQ_PROF 0      // diagnostic build: per-simulation clock64() cycles per event-loop phase
+#endif
+enum { DG_MAXEV = 0, DG_GSCAN, DG_RSCAN, DG_CSCAN, DG_TICKS, DG_WHIT, DG_WMISS, DG_QUIET,
+       DG_P0, DG_N = GFQ_PROF ? DG_P0 + 7 : DG_P0 };
+// GFQ_PROF phases (DG_P0 + k): pool minimum, keep-alive refresh scan, drain (incl. the
+// refresh), monitor ticks, arrivals, completions, expiries + swap-outs
+enum { PF_POOL = 0, PF_REFRESH, PF_DRAIN, PF_TICK, PF_ARR, PF_COMP, PF_EXP };
 
 // event kinds (engine.py:20-23)
 enum { EV_ARRIVAL = 0, EV_COMPLETION = 1, EV_TICK = 2, EV_EXPIRY = 3 };

@@ -252,6 +252,10 @@ struct WarpSim {
     }
     FI int NDEV() const { return ND1 ? 1 : ndev; }
     FI void diag(int k, unsigned v = 1) { if (GFQ_DIAG && lane == 0) ((uint32_t*)(sm + P.L.o_diag))[k] += v; }
+    FI long long pclk() const { return GFQ_PROF ? (long long)clock64() : 0ll; }
+    FI void prof(int k, long long t0) {
+        if (GFQ_PROF && lane == 0) ((uint32_t*)(sm + P.L.o_diag))[DG_P0 + k] += (uint32_t)(clock64() - t0);
+    }
     FI double& UAVG(int d) { return DD(d, DD_UAVG); }
     FI double& SMPT(int d, int i) const { return ((double*)(sm + P.L.o_smp_t))[d * P.L.S + i]; }
     FI double& SMPU(int d, int i) const { return ((double*)(sm + P.L.o_smp_u))[d * P.L.S + i]; }
@@ -1030,6 +1034,11 @@ struct WarpSim {
     FI void refresh_states() {
         if (LIKELY(now < idle_lb)) return;
         diag(DG_RSCAN);
+        const long long p0 = pclk();
+        refresh_scan();
+        prof(PF_REFRESH, p0);
+    }
+    FI void refresh_scan() {
         if (cta_on(nf)) {
             CtaCmd* c = cmd();
             __syncwarp();
@@ -1552,7 +1561,7 @@ struct WarpSim {
         const bool early = P.early_exit && !(G && (P.outputs & (GFQ_WANT_EVENTS | GFQ_WANT_EVICTIONS)));
         #pragma unroll 1
         for (;;) {
-            if (!pmin_ok) pool_min();
+            if (!pmin_ok) { const long long p0 = pclk(); pool_min(); prof(PF_POOL, p0); }
             if (!tick_on) {            // no tick scheduled: the run is ending
                 if (cursor >= n && pmin_slot < 0) break;
                 // exact early exit: only keep-alive rechecks remain, which change
@@ -1571,6 +1580,7 @@ struct WarpSim {
             now = t;
             n_events++;
             bool dr = true;
+            const long long p0 = pclk();
             if (kind == EV_ARRIVAL) {
                 int inv = cursor++;
                 const int fn = RING ? ring_f(inv) : flw(inv);
@@ -1582,6 +1592,7 @@ struct WarpSim {
                 }
                 log_event(t, EV_ARRIVAL, inv);
                 on_arrival(inv, fn);
+                prof(PF_ARR, p0);
             } else if (kind == EV_TICK) {
                 // A run of ticks: while the drain after a tick is provably quiet
                 // (one counted dispatch() call, no state change) and the next
@@ -1617,6 +1628,7 @@ struct WarpSim {
                     n_events++;
                     dr = true;
                 }
+                prof(PF_TICK, p0);
             } else {
                 int slot = pmin_slot;
                 uint32_t meta = ev_meta()[slot];
@@ -1626,16 +1638,18 @@ struct WarpSim {
                     int inv = (int)(pay & 0x7ffffffu);
                     log_event(t, EV_COMPLETION, inv);
                     on_completion(inv, (int)(pay >> 27));
+                    prof(PF_COMP, p0);
                 } else {
                     log_event(t, EV_EXPIRY, (long long)pay);
                     on_expiry((int)pay);
+                    prof(PF_EXP, p0);
                     dr = false;
                 }
             }
             if (UNLIKELY(status)) break;
-            if (dr) drain();
+            if (dr) { const long long p1 = pclk(); drain(); prof(PF_DRAIN, p1); }
             if (UNLIKELY(status)) break;
-            if (!SCRIPTED) swap_out_inactive();
+            if (!SCRIPTED) { const long long p1 = pclk(); swap_out_inactive(); prof(PF_EXP, p1); }
         }
         if (RING) ring_drain();
         if (CSTAGE && (n_comp & 31)) comp_flush(n_comp & 31);
