@@ -251,6 +251,7 @@ __device__ __forceinline__ void sim_setup(WarpSim<POL, ND1, CTA, FG>& w, const P
     w.nf = p.trace_nf[t];
     w.foff = p.foff + p.foff_off[t];
     w.tb = (int)p.tab_off[sim->flowtab];
+    w.mem_int = w.nf > 0 && __ldg(p.memi + w.tb) >= 0;
     w.roff = p.sim_roff[sid];
     w.policy = sim->policy;
     w.scripted_ = sim->device_model == GFQ_DEVMODEL_SCRIPTED;
@@ -266,14 +267,18 @@ __device__ __forceinline__ void sim_setup(WarpSim<POL, ND1, CTA, FG>& w, const P
 template <int POL, bool ND1, bool CTA, bool FG>
 __device__ __forceinline__ void sim_reset_flows(WarpSim<POL, ND1, CTA, FG>& w, const Params& p, int t, int st) {
     double *vt = w.vt(), *lex = w.lex(), *tau = w.tau(), *iat = w.iat(), *larr = w.larr();
-    int *pt = w.pt(), *ph = w.ph(), *infl = w.infl(), *head = w.head(), *done = w.done(), *pend = w.pend();
+    auto *pt = w.pt(), *ph = w.ph(), *infl = w.infl(), *head = w.head(), *done = w.done(), *pend = w.pend();
     uint8_t* fst = w.fst();
     for (int f = t; f < w.nf; f += st) {
         vt[f] = 0.0; lex[f] = 0.0; tau[f] = 0.0; iat[f] = 0.0; larr[f] = 0.0;
-        pt[f] = 0; ph[f] = 0; infl[f] = 0; head[f] = -1; done[f] = 0; pend[f] = 0; fst[f] = 0;
+        pt[f] = 0; ph[f] = 0; infl[f] = 0; head[f] = (typename WarpSim<POL, ND1, CTA, FG>::CI)-1; done[f] = 0; pend[f] = 0; fst[f] = 0;
     }
     uint16_t* cnt = (uint16_t*)(w.fe + p.L.o_cnt);
     for (int i = t; i < 3 * w.ndev * p.L.F; i += st) cnt[i] = 0;
+    if (p.L.o_bmin) {
+        double* bmin = (double*)(w.fe + p.L.o_bmin);
+        for (int i = t; i < p.L.F / 32; i += st) bmin[i] = __longlong_as_double(0x7ff0000000000000ll);
+    }
 }
 
 // Device state reset, the event loop and the per-simulation outputs (one warp).
@@ -412,8 +417,12 @@ __device__ __forceinline__ void run_one(const Params& p, unsigned char* base, un
 #define GFQ_MINB_FG GFQ_MINB
 #endif
 
+#ifndef GFQ_MINB_FAST                     // 1-device warp classes (u16 per-flow state)
+#define GFQ_MINB_FAST GFQ_MINB
+#endif
+
 template <int POL, bool ND1, bool FG>
-__global__ void __launch_bounds__(GFQ_KTHREADS, FG ? GFQ_MINB_FG : GFQ_MINB) k_sim(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(GFQ_KTHREADS, FG ? GFQ_MINB_FG : (ND1 && POL != PB_GENERIC) ? GFQ_MINB_FAST : GFQ_MINB) k_sim(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* slice = smem + (size_t)warp * p.L.bytes;
@@ -618,7 +627,9 @@ struct gfq_handle {
     int32_t n_traces = 0;
     // flow tables
     DBuf warm, cold, mem, share, weight, hist_row, tab_off;
+    DBuf memi;                      // mem_mb as integer MB per row; -1 for every row of a table that is not integral
     std::vector<int64_t> h_tab_off;
+    std::vector<char> h_tab_int;    // per flow table: every mem_mb integral (memi valid)
     std::vector<double> h_mem;
     int32_t n_tabs = 0;
     // device configs, scripted execs
@@ -953,6 +964,7 @@ int gfq_upload_flowtabs(gfq_handle* h, const double* warm_s, const double* cold_
     if ((rc = h->warm.ensure(8 * total)) || (rc = h->cold.ensure(8 * total)) ||
         (rc = h->mem.ensure(8 * total)) || (rc = h->share.ensure(8 * total)) ||
         (rc = h->weight.ensure(8 * total)) || (rc = h->hist_row.ensure(4 * total)) ||
+        (rc = h->memi.ensure(4 * total)) ||
         (rc = h->tab_off.ensure(8 * (n_tabs + 1))))
         return rc;
     if (total) {
@@ -964,9 +976,24 @@ int gfq_upload_flowtabs(gfq_handle* h, const double* warm_s, const double* cold_
         if (hist_row) CK(cudaMemcpyAsync(h->hist_row.p, hist_row, 4 * total, cudaMemcpyHostToDevice, h->xfer));
         else CK(cudaMemsetAsync(h->hist_row.p, 0, 4 * total, h->xfer));
     }
+    // Integral tables: every mem_mb an integer in [1, 2^20].  Then every partial
+    // sum of resident_mb (device.py:114-117) is an integer far below 2^53, each
+    // float addition is exact and CPython's compensated sum() equals the exact
+    // integer total in any order, so the engine sums them lane-parallel.
+    std::vector<int32_t> memi(total);
+    std::vector<char> tab_int(n_tabs);
+    for (int32_t t = 0; t < n_tabs; t++) {
+        bool integral = true;
+        for (int64_t i = off[t]; i < off[t + 1]; i++)
+            integral = integral && mem_mb[i] <= 1048576.0 && mem_mb[i] == floor(mem_mb[i]);
+        for (int64_t i = off[t]; i < off[t + 1]; i++) memi[i] = integral ? (int32_t)mem_mb[i] : -1;
+        tab_int[t] = integral;
+    }
+    if (total) CK(cudaMemcpyAsync(h->memi.p, memi.data(), 4 * total, cudaMemcpyHostToDevice, h->xfer));
     CK(cudaMemcpyAsync(h->tab_off.p, off, 8 * (n_tabs + 1), cudaMemcpyHostToDevice, h->xfer));
     CK(cudaStreamSynchronize(h->xfer));
     h->h_tab_off.assign(off, off + n_tabs + 1);
+    h->h_tab_int = tab_int;
     h->h_mem.assign(mem_mb, mem_mb + total);
     h->n_tabs = n_tabs;
     h->prepared = false;
@@ -1152,14 +1179,21 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     for (int i = 0; i < n_sims; i++) {
         const gfq_sim& s = sims[i];
         int k = 0;
+        // the 1-device fast classes sum resident memory as integers only
+        // (WarpSim::MEMI): a table with a non-integral mem_mb runs generic
+        const bool fast1 = !logs && s.device_model == GFQ_DEVMODEL_DEVICESET && s.n_devices == 1 &&
+                           h->h_tab_int[s.flowtab];
         if (L.cta) {
             k = CLASS_CTA;
-            if (!logs && s.device_model == GFQ_DEVMODEL_DEVICESET && s.n_devices == 1) {
+            if (fast1) {
                 if (s.policy == GFQ_POLICY_MQFQ) k = CLASS_CTA_MQFQ1;
                 else if (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) k = CLASS_CTA_FCFS1;
             }
         } else if (!logs && s.device_model == GFQ_DEVMODEL_DEVICESET) {
-            if (s.n_devices == 1) {
+            // (and, with the flow state in shared memory, u16 per-flow counters:
+            // traces under 65535 arrivals)
+            const int64_t tn = h->h_trace_off[s.trace + 1] - h->h_trace_off[s.trace];
+            if (fast1 && (L.flows_global || tn < 65535)) {
                 k = s.policy == GFQ_POLICY_MQFQ ? 2
                   : (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) ? 3
                   : s.policy == GFQ_POLICY_BATCH ? 4 : 5;
@@ -1181,6 +1215,8 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     // (C2: 18.8 -> 13.9 KB per simulation, 12 -> 16 warps per SM).
     Layout Lk[NCLASS];
     for (int k = 0; k < NCLASS; k++) Lk[k] = L;
+    if (!L.cta && !L.flows_global)
+        for (int k = 2; k <= 5; k++) { Lk[k].i16 = 1; layout_finish(Lk[k]); }
     if (!L.cta && !L.flows_global && c.event_capacity <= 0) {
         const int32_t e_tok = std::max(64, (2 * R * nd + 32 + 31) & ~31);
         for (int k = 3; k <= 5; k++)
@@ -1338,6 +1374,7 @@ static Params make_params(gfq_handle* h) {
     p.trace_off = h->trace_off.as<int64_t>(); p.trace_nf = h->trace_nf.as<int32_t>();
     p.foff_off = h->foff_off.as<int64_t>(); p.foff = h->foff.as<int32_t>(); p.fpos = h->fpos.as<int32_t>();
     p.warm = h->warm.as<double>(); p.cold = h->cold.as<double>(); p.mem = h->mem.as<double>();
+    p.memi = h->memi.as<int32_t>();
     p.share = h->share.as<double>(); p.weight = h->weight.as<double>();
     p.hist_row = h->hist_row.as<int32_t>(); p.tab_off = h->tab_off.as<int64_t>();
     p.dcfg = h->dcfg.as<gfq_device_cfg>(); p.execs = h->execs.as<double>();

@@ -53,7 +53,7 @@ enum { CTA_MAXW = 32 };
 #endif
 struct CtaCmd {
     int32_t op, nf, nev, iarg;     // scan kind, flow count, event slots, use_inf
-    int32_t newly_n, flag, nset, pad1;     // nset: backlogged-set size (large-flow builds)
+    int32_t pad0, pad1, nset, pad2;        // nset: backlogged-set size (large-flow builds)
     double gvt, now;
     unsigned long long pk[CTA_MAXW];
     uint32_t ps[CTA_MAXW];
@@ -70,7 +70,7 @@ struct Layout {
     // F-dependent part ("fe"): per-flow state, dynamic events, per-flow
     // container counts.  Byte offsets from the fe base (8-byte aligned).
     int32_t o_vt, o_lex, o_tau, o_iat, o_larr;          // f64[F]
-    int32_t o_pt, o_ph, o_infl, o_head, o_done, o_pend;  // i32[F]
+    int32_t o_pt, o_ph, o_infl, o_head, o_done, o_pend;  // i32[F] (u16[F] when i16)
     int32_t o_fst;                                       // u8[F]
     int32_t o_ev_t, o_ev_seq, o_ev_meta;                 // f64[E], u32[E], u32[E]
     int32_t o_cnt;                                       // u16[ND][3][F]: gpu-warm, host-warm, running
@@ -94,10 +94,18 @@ struct Layout {
     // warp 0 runs the event loop, the other warps join its O(F) scans
     int32_t cta;
     int32_t bytes;                                       // shared bytes per warp (per CTA in CTA mode)
+    // the six per-flow counters / cursors as u16 (the 1-device warp classes,
+    // traces shorter than 65535 arrivals): a smaller workspace, more
+    // simulations resident per SM
+    int32_t i16;
     // large-flow builds (CTA or flows in global): the set of backlogged flows
     // (pending or in flight) as an unordered list + position index, so the
     // global-VT and candidate scans visit backlogged flows only
     int32_t o_bll, o_blp;                                // u16[F], u16[F] (fe part; 0 = none)
+    // large-flow builds: per 32-flow block, a lower bound on the earliest
+    // keep-alive expiry among the block's idle queues (refresh_states visits
+    // only the blocks whose bound has passed)
+    int32_t o_bmin;                                      // f64[F / 32] (fe part; 0 = none)
 };
 
 struct Params {
@@ -114,6 +122,7 @@ struct Params {
     const int32_t* fpos;           // per trace: arrival positions grouped by flow
     // flow tables (profiles + weights)
     const double *warm, *cold, *mem, *share, *weight;
+    const int32_t* memi;           // mem_mb in integer MB, or -1 for a non-integral table
     const int32_t* hist_row;
     const int64_t* tab_off;
     const gfq_device_cfg* dcfg;
@@ -156,13 +165,14 @@ inline void layout_finish(Layout& L) {
     auto take = [&](int32_t bytes) { int32_t r = o; o = align8(o + bytes); return r; };
     L.o_vt = take(8 * F); L.o_lex = take(8 * F); L.o_tau = take(8 * F);
     L.o_iat = take(8 * F); L.o_larr = take(8 * F);
-    L.o_pt = take(4 * F); L.o_ph = take(4 * F); L.o_infl = take(4 * F);
-    L.o_head = take(4 * F); L.o_done = take(4 * F); L.o_pend = take(4 * F);
+    const int32_t iw = L.i16 ? 2 : 4;
+    L.o_pt = take(iw * F); L.o_ph = take(iw * F); L.o_infl = take(iw * F);
+    L.o_head = take(iw * F); L.o_done = take(iw * F); L.o_pend = take(iw * F);
     L.o_fst = take(F);
     L.o_ev_t = take(8 * E); L.o_ev_seq = take(4 * E); L.o_ev_meta = take(4 * E);
     L.o_cnt = take(2 * 3 * ND * F);
-    if (L.cta || L.flows_global) { L.o_bll = take(2 * F); L.o_blp = take(2 * F); }
-    else L.o_bll = L.o_blp = 0;
+    if (L.cta || L.flows_global) { L.o_bll = take(2 * F); L.o_blp = take(2 * F); L.o_bmin = take(8 * (F / 32)); }
+    else L.o_bll = L.o_blp = L.o_bmin = 0;
     L.fe_bytes = o;
     o = 0;
     auto take16 = [&](int32_t bytes) { o = (o + 15) & ~15; return take(bytes); };

@@ -46,6 +46,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 #include "gfq_layout.h"
 
 namespace gfq {
@@ -179,7 +180,7 @@ FI void ring_init(unsigned char* dev_base, const Layout& L, int lane) {
 }
 
 // CTA-mode scan kinds (the leader warp's command to the helper warps)
-enum { OP_EXIT = 0, OP_GVT, OP_REFRESH, OP_CAND, OP_BATCH, OP_SJF, OP_EVMIN };
+enum { OP_EXIT = 0, OP_GVT, OP_CAND, OP_BATCH, OP_SJF, OP_EVMIN };
 
 // lexicographic (k, s, i) argmin candidate
 struct Arg { u64 k; uint32_t s; int i; };
@@ -215,6 +216,8 @@ struct WarpSim {
     // backlogged flows (pending or in flight: at most the queued invocations
     // plus the tokens out) instead of every touched flow
     static constexpr bool SETS = CTA || FG;
+    // the 1-device fast classes run integral flow tables only (gfq_prepare)
+    static constexpr bool MEMI = !G && ND1;
     const Params& P;
     unsigned char* const sm;   // device part of this warp's state (shared memory)
     unsigned char* const fe;   // flow/event part (shared memory, or global scratch)
@@ -227,15 +230,22 @@ struct WarpSim {
     FI double* tau() const { return (double*)(fe + P.L.o_tau); }
     FI double* iat() const { return (double*)(fe + P.L.o_iat); }
     FI double* larr() const { return (double*)(fe + P.L.o_larr); }
-    FI int* pt() const { return (int*)(fe + P.L.o_pt); }
-    FI int* ph() const { return (int*)(fe + P.L.o_ph); }
-    FI int* infl() const { return (int*)(fe + P.L.o_infl); }
-    FI int* head() const { return (int*)(fe + P.L.o_head); }
-    FI int* done() const { return (int*)(fe + P.L.o_done); }
-    FI int* pend() const { return (int*)(fe + P.L.o_pend); }
+    // per-flow counters / cursors: u16 in the 1-device warp classes (Layout::i16;
+    // gfq_prepare routes traces of 65535+ arrivals elsewhere), i32 otherwise.
+    // head() is only read while the queue has pending work, so its empty
+    // marker (-1, stored as 0xffff) is never compared.
+    static constexpr bool I16 = !G && ND1 && !CTA && !FG;
+    typedef typename std::conditional<I16, uint16_t, int32_t>::type CI;
+    FI CI* pt() const { return (CI*)(fe + P.L.o_pt); }
+    FI CI* ph() const { return (CI*)(fe + P.L.o_ph); }
+    FI CI* infl() const { return (CI*)(fe + P.L.o_infl); }
+    FI CI* head() const { return (CI*)(fe + P.L.o_head); }
+    FI CI* done() const { return (CI*)(fe + P.L.o_done); }
+    FI CI* pend() const { return (CI*)(fe + P.L.o_pend); }
     FI uint8_t* fst() const { return (uint8_t*)(fe + P.L.o_fst); }
     FI uint16_t* BLL() const { return (uint16_t*)(fe + P.L.o_bll); }   // backlogged set (SETS)
     FI uint16_t* BLP() const { return (uint16_t*)(fe + P.L.o_blp); }   // flow -> its slot
+    FI double* BMIN() const { return (double*)(fe + P.L.o_bmin); }     // per-block expiry bound (SETS)
     FI double* ev_t() const { return (double*)(fe + P.L.o_ev_t); }
     FI uint32_t* ev_seq() const { return (uint32_t*)(fe + P.L.o_ev_seq); }
     FI uint32_t* ev_meta() const { return (uint32_t*)(fe + P.L.o_ev_meta); }
@@ -281,6 +291,7 @@ struct WarpSim {
     int64_t toff, roff;
     int tb;
     bool tau_inc;
+    bool mem_int;                      // the flow table's mem_mb are integers (resident_mb)
     const int* foff;
     int n, nf, ndev;
     int policy;
@@ -301,6 +312,7 @@ struct WarpSim {
     FI double warm(int f) const { return __ldg(P.warm + tb + f); }
     FI double cold(int f) const { return __ldg(P.cold + tb + f); }
     FI double mem(int f) const { return __ldg(P.mem + tb + f); }
+    FI uint32_t memi(int f) const { return (uint32_t)__ldg(P.memi + tb + f); }
     FI double share(int f) const { return __ldg(P.share + tb + f); }
     FI double weight(int f) const { return __ldg(P.weight + tb + f); }
 
@@ -410,7 +422,7 @@ struct WarpSim {
     // f = wid*32 + lane + k*nthr), reduced over the warp.
     FI Arg cta_part(int op) {
         Arg a = arg_none();
-        const bool set_op = SETS && op != OP_EVMIN && op != OP_REFRESH;
+        const bool set_op = SETS && op != OP_EVMIN;
         const int lim = op == OP_EVMIN ? nev : set_op ? nbl : nf;
         #pragma unroll 1
         for (int b = wid * 32; b < lim; b += nthr) {
@@ -438,32 +450,6 @@ struct WarpSim {
                 if (in) {
                     u64 k = okey(ev_t()[f]); uint32_t q = ev_seq()[f];
                     if (k < a.k || (k == a.k && q < a.s)) { a.k = k; a.s = q; a.i = f; }
-                }
-            } else {                                        // OP_REFRESH
-                bool idle = false, mk = false;
-                uint8_t st = 0;
-                double le = 0.0, tt = 0.0;
-                if (in) {
-                    st = fst()[f];
-                    idle = (st & (FL_CREATED | FL_INACTIVE)) == FL_CREATED && pt()[f] - done()[f] == 0;
-                    if (idle) { le = lex()[f]; tt = ttl(f); mk = now - le >= tt; }
-                }
-                if (!SCRIPTED) {         // append to the newly-inactive list (order is immaterial)
-                    unsigned bm = __ballot_sync(FULLMASK, mk);
-                    if (bm) {
-                        int pos0 = 0;
-                        if (lane == 0) pos0 = atomicAdd(&cmd()->newly_n, __popc(bm));
-                        pos0 = __shfl_sync(FULLMASK, pos0, 0);
-                        int pos = pos0 + __popc(bm & ((1u << lane) - 1));
-                        if (mk && pos < NEWLY_CAP) NEWLY()[pos] = f;
-                    }
-                }
-                if (mk) {
-                    fst()[f] = (uint8_t)(st | FL_INACTIVE | (SCRIPTED ? 0 : FL_NEWLY));
-                    cmd()->flag = 1;
-                } else if (idle) {
-                    u64 k = okey(expiry_lb(le, tt));
-                    if (k < a.k) a.k = k;
                 }
             }
         }
@@ -638,6 +624,24 @@ struct WarpSim {
     // mem), each a builtin Neumaier sum in list order (replayed via shuffles)
     FI double resident_mb(int d) {
         int np = DV(d, DV_NP);
+        if (MEMI || mem_int) {
+            // integral table (gfq_upload_flowtabs): both builtin sums are exact
+            // integers, so one lane-parallel integer sum gives the same double.
+            // Per lane < 2^32 (entries <= 2^20 MB each); the halves reduce
+            // without overflow and recombine exactly.
+            uint32_t acc = 0;
+            #pragma unroll 1
+            for (int i = lane; i < np; i += 32) {
+                const uint32_t m = PM(d, i);
+                if (pm_th(m) == GFQ_GPU_WARM) acc += memi(pm_fn(m));
+            }
+            const int nr = DV(d, DV_NRUN);
+            #pragma unroll 1
+            for (int r = lane; r < nr; r += 32) acc += memi(RI(d, r, 1));
+            const uint32_t lo = __reduce_add_sync(FULLMASK, acc & 0xffffu);
+            const uint32_t hi = __reduce_add_sync(FULLMASK, acc >> 16);
+            return (double)hi * 65536.0 + (double)lo;
+        }
         PySum a; ps_init(a);
         #pragma unroll 1
         for (int base = 0; base < np; base += 32) {
@@ -1039,16 +1043,7 @@ struct WarpSim {
         prof(PF_REFRESH, p0);
     }
     FI void refresh_scan() {
-        if (cta_on(nf)) {
-            CtaCmd* c = cmd();
-            __syncwarp();
-            if (lane == 0) { c->newly_n = newly_n; c->flag = 0; }
-            Arg a = cta_scan(OP_REFRESH);
-            newly_n = c->newly_n;
-            if (c->flag && !SCRIPTED) any_newly = true;
-            idle_lb = a.k == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_key(a.k);
-            return;
-        }
+        if (SETS) { refresh_blocks(); return; }   // every CTA build is a SETS build
         u64 lbk = ~0ull;
         bool newly = false;
         #pragma unroll 1
@@ -1079,6 +1074,63 @@ struct WarpSim {
         __syncwarp();
         if (wor32(newly) && !SCRIPTED) any_newly = true;
         u64 m = wmin64(lbk);
+        idle_lb = m == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_key(m);
+    }
+
+    // Large-flow builds: refresh_states over the 32-flow blocks whose expiry
+    // bound has passed.  BMIN[b] is a lower bound on expiry_lb() of every idle
+    // queue in block b: lowered when a queue of the block drains
+    // (policy_on_completion), never raised except here, where the block is
+    // rescanned and gets its exact bound.  A queue can only be expired when
+    // now >= its expiry_lb >= its block's bound, so every expired queue lies
+    // in a visited block and the marks equal the full scan's; idle_lb becomes
+    // the minimum over all the blocks' bounds (still a valid lower bound).
+    // One warp does it all (the leader in CTA builds).
+    FI void refresh_blocks() {
+        const int nb = (nf + 31) >> 5;
+        u64 lbk = ~0ull;
+        bool newly = false;
+        #pragma unroll 1
+        for (int base = 0; base < nb; base += 32) {
+            const int b = base + lane;
+            const double bm = b < nb ? BMIN()[b] : __longlong_as_double(0x7ff0000000000000ll);
+            const bool hit = b < nb && bm <= now;
+            if (!hit) { u64 k = okey(bm); if (k < lbk) lbk = k; }
+            unsigned hm = __ballot_sync(FULLMASK, hit);
+            #pragma unroll 1
+            while (hm) {
+                const int bb = base + __ffs(hm) - 1; hm &= hm - 1;
+                const int f = bb * 32 + lane;
+                bool idle = false, mk = false;
+                uint8_t s = 0;
+                double le = 0.0, tt = 0.0;
+                if (f < nf) {
+                    s = fst()[f];
+                    idle = (s & (FL_CREATED | FL_INACTIVE)) == FL_CREATED && pt()[f] - done()[f] == 0;
+                    if (idle) { le = lex()[f]; tt = ttl(f); mk = now - le >= tt; }
+                }
+                if (!SCRIPTED) {
+                    unsigned bm2 = __ballot_sync(FULLMASK, mk);
+                    int pos = newly_n + __popc(bm2 & ((1u << lane) - 1));
+                    if (mk && pos < NEWLY_CAP) NEWLY()[pos] = f;
+                    newly_n += __popc(bm2);
+                }
+                u64 k = ~0ull;
+                if (mk) {
+                    fst()[f] = (uint8_t)(s | FL_INACTIVE | (SCRIPTED ? 0 : FL_NEWLY));
+                    newly = true;
+                } else if (idle) {
+                    k = okey(expiry_lb(le, tt));
+                }
+                const u64 m = wmin64(k);
+                __syncwarp();
+                if (lane == 0) BMIN()[bb] = m == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_key(m);
+                if (m < lbk) lbk = m;
+            }
+        }
+        __syncwarp();
+        if (wor32(newly) && !SCRIPTED) any_newly = true;
+        const u64 m = wmin64(lbk);
         idle_lb = m == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_key(m);
     }
 
@@ -1253,7 +1305,7 @@ struct WarpSim {
     FI void policy_on_completion(int fn, double exec_s) {
         tot_infl--;
         int dn = done()[fn] + 1;
-        if (FCFS) { fcfs_infl -= 1; ust(done()[fn], dn); return; }
+        if (FCFS) { fcfs_infl -= 1; ust(done()[fn], (CI)dn); return; }
         int inf = infl()[fn] - 1;
         double tm = tau()[fn];
         tm = tm + (exec_s - tm) / (double)dn;            // tau.count == completions
@@ -1262,7 +1314,9 @@ struct WarpSim {
         if (MQFQ) lex()[fn] = now;
         if (MQFQ && pt()[fn] == dn) {                     // queue drained (idle)
             if (gmin_ok && okey(vt()[fn]) == gmin) gmin_ok = false;          // (A)
-            idle_lb = pymin(idle_lb, expiry_lb(now, ttl(fn)));               // (B)
+            const double lb = expiry_lb(now, ttl(fn));
+            idle_lb = pymin(idle_lb, lb);                                    // (B)
+            if (SETS) ust(BMIN()[fn >> 5], pymin(BMIN()[fn >> 5], lb));
         }
     }
 
@@ -1322,6 +1376,24 @@ struct WarpSim {
         if (LIKELY(!any_newly)) return;
         any_newly = false;
         if (G && (P.outputs & GFQ_WANT_EVICTIONS)) swap_out_log();
+        if (newly_n <= NEWLY_CAP) {
+            // no idle container of any listed function on any device: swap_out
+            // and mark_evictable change nothing, and a later unmark_evictable
+            // finds nothing to clear (containers pooled later are not
+            // evictable), so only the NEWLY flags go
+            bool has = false;
+            if (lane < newly_n) {
+                const int f = NEWLY()[lane];
+                #pragma unroll 1
+                for (int d = 0; d < NDEV(); d++) has |= (CNT(d, 0, f) | CNT(d, 1, f)) != 0;
+            }
+            if (!__any_sync(FULLMASK, has)) {
+                if (lane < newly_n) { const int f = NEWLY()[lane]; fst()[f] = (uint8_t)(fst()[f] & ~FL_NEWLY); }
+                __syncwarp();
+                newly_n = 0;
+                return;
+            }
+        }
         #pragma unroll 1
         for (int d = 0; d < NDEV(); d++) {
             int np = DV(d, DV_NP);
