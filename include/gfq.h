@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define GFQ_ABI_VERSION 2
+#define GFQ_ABI_VERSION 3
 
 /* ---- status codes ---------------------------------------------------- */
 #define GFQ_OK        0
@@ -202,6 +202,17 @@ enum gfq_output_id {
                                   (GFQ_WANT_EVICTIONS; rows <= arrivals)         */
     GFQ_OUT_EVICT_META,        /* int32  [invocations] flow << 4 | device         */
     GFQ_OUT_EVICT_COUNT,       /* int64  [sims]                                   */
+    GFQ_OUT_DSP_EVENT,         /* int32  [invocations] per dispatch row: the
+                                  1-based index of the processed event whose
+                                  drain made it (generic build, i.e. with
+                                  GFQ_WANT_AUDIT / EVENTS / EVICTIONS; 0
+                                  otherwise) -- Simulation.step() replay      */
+    GFQ_OUT_EVICT_EVENT,       /* int32  [invocations] per eviction row: the
+                                  processed event that logged it             */
+    GFQ_OUT_REC_START_TAG,     /* double [invocations] Invocation.start_tag set
+                                  by FlowQueue.enqueue (core.py:131-134):
+                                  MQFQ in the generic build with
+                                  GFQ_WANT_RECORDS; 0 otherwise              */
     GFQ_OUT_COUNT_
 };
 

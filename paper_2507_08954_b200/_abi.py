@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 GFQ_OK, GFQ_EINVAL, GFQ_ERUNTIME, GFQ_ECUDA, GFQ_ENOMEM = 0, 1, 2, 3, 4
 
 POLICY_MQFQ, POLICY_FCFS, POLICY_BATCH, POLICY_SJF, POLICY_FCFS_NAIVE = 0, 1, 2, 3, 4
@@ -41,8 +41,8 @@ WANT_STATS, WANT_RECORDS, WANT_DISPATCH, WANT_AUDIT, WANT_EVENTS, WANT_HIST, WAN
  OUT_UTIL_ROWS, OUT_UTIL_META, OUT_BACKLOG_TIME, OUT_BACKLOG_META,
  OUT_BACKLOG_COUNT, OUT_EVENT_TIME, OUT_EVENT_META, OUT_EVENT_COUNT,
  OUT_HIST, OUT_FAIR_ROWS, OUT_FAIR_META, OUT_FAIR_OFF, OUT_FAIR_COUNT,
- OUT_EVICT_TIME, OUT_EVICT_META, OUT_EVICT_COUNT,
- OUT_COUNT_) = range(36)
+ OUT_EVICT_TIME, OUT_EVICT_META, OUT_EVICT_COUNT, OUT_DSP_EVENT, OUT_EVICT_EVENT,
+ OUT_REC_START_TAG, OUT_COUNT_) = range(39)
 
 
 class DeviceCfg(C.Structure):

@@ -275,6 +275,10 @@ __device__ __forceinline__ void sim_reset_flows(WarpSim<POL, ND1, CTA, FG>& w, c
     }
     uint16_t* cnt = (uint16_t*)(w.fe + p.L.o_cnt);
     for (int i = t; i < 3 * w.ndev * p.L.F; i += st) cnt[i] = 0;
+    if (p.L.o_lst) {
+        double* lst = (double*)(w.fe + p.L.o_lst);
+        for (int f = t; f < w.nf; f += st) lst[f] = 0.0;
+    }
     if (p.L.o_bmin) {
         double* bmin = (double*)(w.fe + p.L.o_bmin);
         for (int i = t; i < p.L.F / 32; i += st) bmin[i] = __longlong_as_double(0x7ff0000000000000ll);
@@ -678,7 +682,9 @@ static const int32_t kOutBytes[GFQ_OUT_COUNT_] = {
     8, 8, 8,                  // event time/meta/count
     8,                        // hist
     8, 8, 8, 8,               // fairness rows/meta/offsets/counts
-    8, 4, 8};                 // eviction log time/meta/count
+    8, 4, 8,                  // eviction log time/meta/count
+    4, 4,                     // dispatch-row / eviction-row event index
+    8};                       // start tags
 
 extern "C" {
 
@@ -1119,6 +1125,10 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     L.E = c.event_capacity > 0 ? c.event_capacity : std::max(64, ((2 * max_nf + 2 * R * nd + 32) + 31) & ~31);
     L.flows_global = 0;
     L.cta = 0;
+    // records with the logs: every simulation runs the generic build, which
+    // then also keeps FlowQueue.last_start_tag and writes each start tag
+    L.lst = (c.outputs & GFQ_WANT_RECORDS) &&
+            (c.outputs & (GFQ_WANT_AUDIT | GFQ_WANT_EVENTS | GFQ_WANT_EVICTIONS));
     layout_finish(L);
     // Large flow counts (fewer than 4 warp-simulations' workspaces fit an SM's
     // shared memory, or GFQ_FLAG_CTA): one simulation per CTA, its scans split
@@ -1295,10 +1305,11 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
             if ((rc = alloc_out(h, id, flows))) return rc;
     if (c.outputs & GFQ_WANT_RECORDS)
         for (int id : {GFQ_OUT_REC_DISPATCH, GFQ_OUT_REC_COMPLETE, GFQ_OUT_REC_STATE, GFQ_OUT_REC_DEVICE,
-                       GFQ_OUT_REC_ORDER, GFQ_OUT_REC_PURE})
+                       GFQ_OUT_REC_ORDER, GFQ_OUT_REC_PURE, GFQ_OUT_REC_START_TAG})
             if ((rc = alloc_out(h, id, recs))) return rc;
     if (c.outputs & GFQ_WANT_DISPATCH)
-        for (int id : {GFQ_OUT_DSP_INV, GFQ_OUT_DSP_VT_BEFORE, GFQ_OUT_DSP_GVT, GFQ_OUT_DSP_QLEN, GFQ_OUT_DSP_INFLIGHT})
+        for (int id : {GFQ_OUT_DSP_INV, GFQ_OUT_DSP_VT_BEFORE, GFQ_OUT_DSP_GVT, GFQ_OUT_DSP_QLEN, GFQ_OUT_DSP_INFLIGHT,
+                       GFQ_OUT_DSP_EVENT})
             if ((rc = alloc_out(h, id, recs))) return rc;
     if (c.outputs & GFQ_WANT_AUDIT) {
         if (c.audit_util_cap <= 0) c.audit_util_cap = 1 << 16;
@@ -1312,6 +1323,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     }
     if (c.outputs & GFQ_WANT_EVICTIONS)
         if ((rc = alloc_out(h, GFQ_OUT_EVICT_TIME, recs)) || (rc = alloc_out(h, GFQ_OUT_EVICT_META, recs)) ||
+            (rc = alloc_out(h, GFQ_OUT_EVICT_EVENT, recs)) ||
             (rc = alloc_out(h, GFQ_OUT_EVICT_COUNT, n_sims)))
             return rc;
     if (c.outputs & GFQ_WANT_EVENTS) {
@@ -1397,6 +1409,7 @@ static Params make_params(gfq_handle* h) {
     p.rec_dispatch = h->out[GFQ_OUT_REC_DISPATCH].as<double>();
     p.rec_complete = h->out[GFQ_OUT_REC_COMPLETE].as<double>();
     p.rec_pure = h->out[GFQ_OUT_REC_PURE].as<double>();
+    p.rec_stag = h->out[GFQ_OUT_REC_START_TAG].as<double>();
     p.rec_state = h->out[GFQ_OUT_REC_STATE].as<int8_t>();
     p.rec_device = h->out[GFQ_OUT_REC_DEVICE].as<int8_t>();
     p.rec_order = h->out[GFQ_OUT_REC_ORDER].as<int32_t>();
@@ -1405,6 +1418,7 @@ static Params make_params(gfq_handle* h) {
     p.dsp_gvt = h->out[GFQ_OUT_DSP_GVT].as<double>();
     p.dsp_qlen = h->out[GFQ_OUT_DSP_QLEN].as<int32_t>();
     p.dsp_infl = h->out[GFQ_OUT_DSP_INFLIGHT].as<int32_t>();
+    p.dsp_ev = h->out[GFQ_OUT_DSP_EVENT].as<int32_t>();
     p.util_rows = h->out[GFQ_OUT_UTIL_ROWS].as<double>();
     p.util_meta = h->out[GFQ_OUT_UTIL_META].as<int32_t>();
     p.audit_util_cap = h->cfg.audit_util_cap;
@@ -1418,6 +1432,7 @@ static Params make_params(gfq_handle* h) {
     p.event_log_cap = h->cfg.event_log_cap;
     p.evict_time = h->out[GFQ_OUT_EVICT_TIME].as<double>();
     p.evict_meta = h->out[GFQ_OUT_EVICT_META].as<int32_t>();
+    p.evict_ev = h->out[GFQ_OUT_EVICT_EVENT].as<int32_t>();
     p.evict_count = h->out[GFQ_OUT_EVICT_COUNT].as<int64_t>();
     p.hist = h->out[GFQ_OUT_HIST].as<unsigned long long>();
     p.hist_rows = h->cfg.hist_rows; p.hist_bins = h->cfg.hist_bins;
@@ -1435,6 +1450,10 @@ int gfq_launch(gfq_handle* h, void* stream) {
     CK(cudaMemsetAsync(h->work.p, 0, 4 * NCLASS, st));   // one work counter per class
     if (h->cfg.outputs & GFQ_WANT_HIST)
         CK(cudaMemsetAsync(h->out[GFQ_OUT_HIST].p, 0, 8 * h->out_n[GFQ_OUT_HIST], st));
+    if (h->cfg.outputs & GFQ_WANT_DISPATCH)        // written by the generic build only
+        CK(cudaMemsetAsync(h->out[GFQ_OUT_DSP_EVENT].p, 0, 4 * h->out_n[GFQ_OUT_DSP_EVENT], st));
+    if (h->cfg.outputs & GFQ_WANT_RECORDS)         // MQFQ arrivals in the generic build only
+        CK(cudaMemsetAsync(h->out[GFQ_OUT_REC_START_TAG].p, 0, 8 * h->out_n[GFQ_OUT_REC_START_TAG], st));
     cudaEvent_t* re = &h->ring[3 * h->ring_next];
     CK(cudaEventRecord(h->ev[0], st));
     CK(cudaEventRecord(re[0], st));

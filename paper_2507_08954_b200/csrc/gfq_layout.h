@@ -106,6 +106,10 @@ struct Layout {
     // keep-alive expiry among the block's idle queues (refresh_states visits
     // only the blocks whose bound has passed)
     int32_t o_bmin;                                      // f64[F / 32] (fe part; 0 = none)
+    // FlowQueue.last_start_tag per flow: batches that ask for records together
+    // with the logs (the generic build: Simulation.step() replays start tags)
+    int32_t lst;                                         // flag
+    int32_t o_lst;                                       // f64[F] (fe part; 0 = none)
 };
 
 struct Params {
@@ -143,12 +147,15 @@ struct Params {
     double* comp_lat; int32_t* comp_meta;
     int32_t* comp_pos;             // completion rank -> trace position (GFQ_WANT_RECORDS)
     double* rec_dispatch; double* rec_complete; double* rec_pure;
+    double* rec_stag;              // Invocation.start_tag (generic build, Layout::lst)
     int8_t* rec_state; int8_t* rec_device; int32_t* rec_order;
     int32_t* dsp_inv; double* dsp_vt; double* dsp_gvt; int32_t* dsp_qlen; int32_t* dsp_infl;
+    int32_t* dsp_ev;               // generic build: processed-event index of each dispatch row
     double* util_rows; int32_t* util_meta; int64_t audit_util_cap;
     double* backlog_time; int32_t* backlog_meta; int64_t* backlog_count; int64_t audit_backlog_cap;
     double* event_time; int64_t* event_meta; int64_t* event_count; int64_t event_log_cap;
     double* evict_time; int32_t* evict_meta; int64_t* evict_count;   // at the sim's record offset
+    int32_t* evict_ev;             // processed-event index of each eviction row
     unsigned long long* hist; int32_t hist_rows, hist_bins; double hist_lo, hist_hi;
     int32_t* work;                 // work-queue counter
     double* rscratch;              // reducer: per-warp record scratch (rscratch_per_warp doubles)
@@ -173,6 +180,7 @@ inline void layout_finish(Layout& L) {
     L.o_cnt = take(2 * 3 * ND * F);
     if (L.cta || L.flows_global) { L.o_bll = take(2 * F); L.o_blp = take(2 * F); L.o_bmin = take(8 * (F / 32)); }
     else L.o_bll = L.o_blp = L.o_bmin = 0;
+    L.o_lst = L.lst ? take(8 * F) : 0;
     L.fe_bytes = o;
     o = 0;
     auto take16 = [&](int32_t bytes) { o = (o + 15) & ~15; return take(bytes); };

@@ -1211,6 +1211,7 @@ struct WarpSim {
                 int64_t o = roff + k;
                 P.dsp_inv[o] = inv; P.dsp_vt[o] = vt_before; P.dsp_gvt[o] = g;
                 P.dsp_qlen[o] = qlen; P.dsp_infl[o] = infl_after;
+                if (G) P.dsp_ev[o] = n_events;         // Simulation.step() replay
             }
             __syncwarp();                    // reconverge after the lane-0 write
         }
@@ -1294,6 +1295,13 @@ struct WarpSim {
                 u64 k = okey(v);
                 if (k < gmin) gmin = k;
             }
+            if (G && MQFQ && P.L.o_lst) {                 // FlowQueue.enqueue start tag, core.py:131-134
+                double* lst = (double*)(fe + P.L.o_lst);
+                const double stag = pymax(lst[fn], v + (double)pe * tau()[fn]);
+                ust(lst[fn], stag);
+                if (lane == 0) P.rec_stag[roff + inv] = stag;
+                __syncwarp();
+            }
         }
         USYNC();
         fst()[fn] = s; pt()[fn] = p0 + 1; pend()[fn] = pe + 1;
@@ -1340,7 +1348,7 @@ struct WarpSim {
         const int k = n_evict++;
         if ((P.outputs & GFQ_WANT_EVICTIONS) && lane == 0) {
             const int64_t o = P.sim_roff[sid] + k;
-            P.evict_time[o] = now; P.evict_meta[o] = (fn << 4) | d;
+            P.evict_time[o] = now; P.evict_meta[o] = (fn << 4) | d; P.evict_ev[o] = n_events;
         }
     }
     // Device.swap_out's log rows (device.py:270-275) for this call's newly

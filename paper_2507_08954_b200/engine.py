@@ -46,6 +46,7 @@ _OUT_DTYPES = {
     _abi.OUT_FAIR_ROWS: np.float64, _abi.OUT_FAIR_META: np.int64, _abi.OUT_FAIR_OFF: np.int64,
     _abi.OUT_FAIR_COUNT: np.int64, _abi.OUT_EVICT_TIME: np.float64,
     _abi.OUT_EVICT_META: np.int32, _abi.OUT_EVICT_COUNT: np.int64,
+    _abi.OUT_DSP_EVENT: np.int32, _abi.OUT_EVICT_EVENT: np.int32, _abi.OUT_REC_START_TAG: np.float64,
 }
 
 _POLICY = {"mqfq": _abi.POLICY_MQFQ, "fcfs": _abi.POLICY_FCFS, "batch": _abi.POLICY_BATCH,
@@ -413,6 +414,8 @@ class BatchResult:
                 "state": self.get(_abi.OUT_REC_STATE)[a:b],
                 "device": self.get(_abi.OUT_REC_DEVICE)[a:b],
                 "pure": self.get(_abi.OUT_REC_PURE)[a:b],
+                # FlowQueue start tags (MQFQ, generic build with the logs; else 0)
+                "start_tag": self.get(_abi.OUT_REC_START_TAG)[a:b],
                 "order": order, "n": n_done}
 
     def completion_order(self, i: int) -> np.ndarray:
@@ -430,7 +433,9 @@ class BatchResult:
                 "vt_before": self.get(_abi.OUT_DSP_VT_BEFORE)[a:a + k],
                 "gvt": self.get(_abi.OUT_DSP_GVT)[a:a + k],
                 "qlen": self.get(_abi.OUT_DSP_QLEN)[a:a + k],
-                "inflight": self.get(_abi.OUT_DSP_INFLIGHT)[a:a + k]}
+                "inflight": self.get(_abi.OUT_DSP_INFLIGHT)[a:a + k],
+                # generic build: the processed event whose drain made each row
+                "event": self.get(_abi.OUT_DSP_EVENT)[a:a + k]}
 
     def _cap(self, oid: int, per: int) -> int:
         return int(self.get(oid).shape[0]) // (per * max(self.n_sims, 1))
@@ -449,13 +454,16 @@ class BatchResult:
         m = self.get(_abi.OUT_BACKLOG_META).reshape(-1, cap)[i, :k]
         return t, m
 
-    def eviction_rows(self, i: int):
+    def eviction_rows(self, i: int, events: bool = False):
         """(time, device, flow) arrays of sim i's Device.eviction_log rows,
-        all devices interleaved in the order they were logged."""
+        all devices interleaved in the order they were logged (+ the index of
+        the processed event that logged each, with events=True)."""
         a = int(self.rec_off[i])
         k = int(self.get(_abi.OUT_EVICT_COUNT)[i])
         t = self.get(_abi.OUT_EVICT_TIME)[a:a + k]
         m = self.get(_abi.OUT_EVICT_META)[a:a + k].astype(np.int64)
+        if events:
+            return t, m & 15, m >> 4, self.get(_abi.OUT_EVICT_EVENT)[a:a + k]
         return t, m & 15, m >> 4
 
     def event_rows(self, i: int):
@@ -622,11 +630,21 @@ class Simulation:
     Construction validates like the reference (unknown functions and
     decreasing arrival times raise ``ValueError``).  On first ``step()`` or
     ``run()`` the whole simulation runs on the GPU in parity mode (processed-
-    event log, records, dispatch rows, audit); ``step()`` then replays the
-    processed events in order as the reference's ``(time, kind, payload)``
-    tuples -- an ``Invocation`` for arrivals, its ``uid`` for completions,
+    event log, records, dispatch rows with the event that made each, audit,
+    eviction log).  ``step()`` then replays it event by event and leaves the
+    observable state where the reference's ``step()`` leaves it
+    (engine.py:99-197): it returns the reference's ``(time, kind, payload)``
+    tuple -- the ``Invocation`` for arrivals, its ``uid`` for completions,
     ``None`` for monitor ticks, the function name for keep-alive expiries --
-    advancing ``now`` and appending each completion's ``InvocationRecord``.
+    advances ``now``; a completion appends its ``InvocationRecord`` and
+    ``audit.exec`` row and stamps ``complete_s``; backlog transitions and
+    monitor ticks append their ``audit.backlog`` / ``audit.util`` rows; the
+    dispatches of the event's drain stamp their invocations' ``dispatch_s`` /
+    ``start_state`` and append their ``DispatchAudit`` rows to
+    ``policy.dispatch_log``; the event's evictions go to each device's
+    ``eviction_log``.  ``run()`` then shares ``policy.dispatch_log`` as
+    ``audit.dispatches`` (engine.py:118).  The policy's and devices' internal
+    queues and pools are not replayed.
     """
 
     def __init__(self, trace, profiles, policy, devices, tau_includes_overheads: bool = False,
@@ -660,23 +678,33 @@ class Simulation:
         res = _run_one(eng, sim, pt.n, _abi.WANT_STATS | _abi.WANT_RECORDS | _abi.WANT_DISPATCH |
                        _abi.WANT_AUDIT | _abi.WANT_EVENTS | _abi.WANT_EVICTIONS, False,
                        event_log_cap=cap, audit_util_cap=cap, audit_backlog_cap=2 * pt.n + 2)
-        self._result = to_sim_result(res, 0, pt)
-        _append_eviction_logs(self.devices, res, 0, pt.names)
+        full = to_sim_result(res, 0, pt)
         rec = res.records(0)
-        for p, inv in enumerate(self._inv):
-            inv.dispatch_s = float(rec["dispatch"][p])
-            inv.complete_s = float(rec["complete"][p])
-            inv.start_state = STATE_BY_CODE[int(rec["state"][p])]
-        self._rec_of = {}
+        self._rec_dispatch = rec["dispatch"].tolist()
+        self._rec_state = [STATE_BY_CODE[int(x)] for x in rec["state"].tolist()]
+        self._stag = rec["start_tag"].tolist()
         order = rec["order"]
-        for p in range(pt.n):
-            self._rec_of[p] = self._result.records[int(order[p])]
+        self._rec_of = {p: full.records[int(order[p])] for p in range(pt.n)}
+        self._exec_of = {p: full.audit.exec[int(order[p])] for p in range(pt.n)}
+        # dispatch rows and eviction rows, bucketed by the processed event
+        # (1-based) whose drain / swap-out made them
+        dr = res.dispatch_rows(0)
+        self._disp_of = {}
+        for j, (ev, p) in enumerate(zip(dr["event"].tolist(), dr["inv"].tolist())):
+            self._disp_of.setdefault(ev, []).append((p, full.audit.dispatches[j]))
+        t, d, f, e = res.eviction_rows(0, events=True)
+        self._evict_of = {}
+        for tt, dd, ff, ee in zip(t.tolist(), d.tolist(), f.tolist(), e.tolist()):
+            self._evict_of.setdefault(ee, []).append((dd, (tt, pt.names[ff])))
+        self._util_rows = full.audit.util
+        self._backlog = {}
+        self._ndev = max(len(dcfgs), 1)
         et, em = res.event_rows(0)
         evs = []
         for t, m in zip(et.tolist(), em.tolist()):
             kind, pay = m & 3, m >> 2
             if kind == ARRIVAL:
-                evs.append((t, kind, self._inv[pay]))
+                evs.append((t, kind, self._inv[pay], pay))
             elif kind == COMPLETION:
                 evs.append((t, kind, self._inv[pay].uid, pay))
             elif kind == MONITOR_TICK:
@@ -684,6 +712,15 @@ class Simulation:
             else:
                 evs.append((t, kind, pt.names[pay]))
         self._events = evs
+        self._result = full
+
+    def _backlog_change(self, t, fn, delta) -> None:
+        """_backlog_change, engine.py:199-207: the row of a 0 -> 1 or 1 -> 0
+        transition (the GPU run's rows, in the same order)."""
+        c = self._backlog.get(fn, 0) + delta
+        self._backlog[fn] = c
+        if (delta > 0 and c == 1) or (delta < 0 and c == 0):
+            self.audit.backlog.append((t, fn, delta > 0))
 
     def step(self):
         """Process the earliest event; returns (time, kind, payload) or None."""
@@ -692,26 +729,42 @@ class Simulation:
             return None
         ev = self._events[self._pos]
         self._pos += 1
-        self.now = ev[0]
-        if ev[1] == COMPLETION:
-            self.records.append(self._rec_of[ev[3]])
+        k = self._pos                                   # 1-based processed-event index
+        self.now = t = ev[0]
+        if ev[1] == ARRIVAL:
+            ev[2].start_tag = self._stag[ev[3]]         # FlowQueue.enqueue, core.py:131-134
+            self._backlog_change(t, ev[2].function, +1)
             ev = ev[:3]
-        if self._pos == len(self._events):
-            self._finish()
+        elif ev[1] == COMPLETION:
+            p = ev[3]
+            self._inv[p].complete_s = t
+            self.records.append(self._rec_of[p])
+            self._backlog_change(t, self._inv[p].function, -1)
+            self.audit.exec.append(self._exec_of[p])
+            ev = ev[:3]
+        elif ev[1] == MONITOR_TICK:
+            u0 = len(self.audit.util)
+            self.audit.util.extend(self._util_rows[u0:u0 + self._ndev])
+        log = getattr(self.policy, "dispatch_log", None)
+        for p, row in self._disp_of.get(k, ()):
+            inv = self._inv[p]
+            inv.dispatch_s = self._rec_dispatch[p]
+            inv.start_state = self._rec_state[p]
+            (log if isinstance(log, list) else self.audit.dispatches).append(row)
+        if k in self._evict_of:
+            devs = list(self.devices)
+            for d, row in self._evict_of[k]:
+                elog = getattr(devs[d], "eviction_log", None)
+                if isinstance(elog, list):
+                    elog.append(row)
         return ev
-
-    def _finish(self) -> None:
-        a = self._result.audit
-        self.audit.backlog, self.audit.util, self.audit.exec = a.backlog, a.util, a.exec
-        _share_dispatch_log(self.policy, a)
-        self.audit.dispatches = a.dispatches
 
     def run(self) -> SimResult:
         while self.step() is not None:
             pass
-        self._ensure()
-        if not self._events:
-            self._finish()
+        log = getattr(self.policy, "dispatch_log", None)
+        if isinstance(log, list):
+            self.audit.dispatches = log                  # engine.py:118
         return SimResult(records=self.records, audit=self.audit)
 
 

@@ -149,3 +149,61 @@ def test_reference_validation_errors(ref):
     with pytest.raises(ValueError, match="non-decreasing"):
         run_simulation(Trace(entries=[(1.0, "fft"), (0.5, "fft")], duration_s=1.0), prof, pol,
                        DeviceSet([DeviceConfig()]))
+
+
+@pytest.mark.parametrize("name", ["default", "two_devices", "evicting", "fcfs", "sjf"])
+def test_simulation_state_between_steps(ref, name):
+    """After EVERY step() the replayed observable state equals the reference's:
+    now, records, policy.dispatch_log, audit.backlog / util / exec, each
+    device's eviction_log, and the arrival Invocations' start_tag (at their
+    arrival step) and dispatch_s / complete_s / start_state (as they happen)."""
+    from gpufairq.engine import Simulation as RefSim
+    from paper_2507_08954_b200.engine import Simulation as GpuSim
+
+    def last(xs):
+        return tuple(xs[-1]) if xs else None
+
+    def snap(sim, pol, dev):
+        log = pol.dispatch_log
+        d = log[-1] if log else None
+        r = sim.records[-1] if sim.records else None
+        return (sim.now, len(sim.records),
+                None if r is None else (r.function, r.arrival_s, r.dispatch_s, r.complete_s,
+                                        r.start_state, r.device),
+                len(log), None if d is None else (d.now, d.function, d.vt_before, d.global_vt,
+                                                  d.queue_len, d.in_flight, d.device,
+                                                  d.start_state),
+                len(sim.audit.backlog), last(sim.audit.backlog),
+                len(sim.audit.util), last(sim.audit.util),
+                len(sim.audit.exec), last(sim.audit.exec),
+                tuple(len(x.eviction_log) for x in dev), tuple(last(x.eviction_log) for x in dev))
+
+    def inv_state(invs):
+        return [(i.function, i.arrival_s, i.start_tag, i.dispatch_s, i.complete_s,
+                 None if i.start_state is None else i.start_state.value) for i in invs]
+
+    c = CASES[name]
+    tr, p, rpol, rdev = _inputs(ref, c)
+    rs = RefSim(tr, p, rpol, rdev)
+    tr, p, gpol, gdev = _inputs(ref, c)
+    gs = GpuSim(tr, p, gpol, gdev)
+    rinv, ginv = [], []
+    k = 0
+    while True:
+        a, b = rs.step(), gs.step()
+        assert (a is None) == (b is None), k
+        if a is None:
+            break
+        assert (a[0], a[1]) == (b[0], b[1]), k
+        if a[1] == 0:
+            rinv.append(a[2])
+            ginv.append(b[2])
+            assert a[2].start_tag == b[2].start_tag, (k, a[2], b[2])
+        assert snap(rs, rpol, rdev) == snap(gs, gpol, gdev), k
+        if k % 97 == 0:
+            assert inv_state(rinv) == inv_state(ginv), k
+        k += 1
+    assert inv_state(rinv) == inv_state(ginv)
+    want, got = rs.run(), gs.run()
+    assert want.audit.dispatches is rpol.dispatch_log and got.audit.dispatches is gpol.dispatch_log
+    assert k > 1000
