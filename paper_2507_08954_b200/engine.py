@@ -769,36 +769,33 @@ class Simulation:
 
 
 def to_sim_result(res: BatchResult, i: int, pt: PackedTrace) -> SimResult:
+    """Reference-shaped SimResult of simulation i (records in completion
+    order, DispatchAudit rows, audit.exec / util / backlog).  The arrays are
+    turned into Python lists once, and the rows are built from those."""
     names = pt.names
     rec = res.records(i)
     k = int(res.counters[i, 2])
-    comp = res.completion_order(i)
-    records = []
-    exe = []
-    for p in comp.tolist():
-        fn = names[int(pt.flow[p])]
-        records.append(InvocationRecord(fn, float(pt.arrival[p]), float(rec["dispatch"][p]),
-                                        float(rec["complete"][p]),
-                                        STATE_BY_CODE[int(rec["state"][p])].value,
-                                        int(rec["device"][p])))
-        exe.append((fn, float(rec["dispatch"][p]), float(rec["complete"][p]),
-                    float(rec["pure"][p])))
+    comp = res.completion_order(i).tolist()
+    fname = [names[f] for f in pt.flow.tolist()]
+    arr = pt.arrival.tolist()
+    d_s, c_s, pure = rec["dispatch"].tolist(), rec["complete"].tolist(), rec["pure"].tolist()
+    sv = [s.value for s in STATE_BY_CODE]
+    st = [sv[x] for x in rec["state"].tolist()]
+    dv = rec["device"].tolist()
+    records = [InvocationRecord(fname[p], arr[p], d_s[p], c_s[p], st[p], dv[p]) for p in comp]
+    exe = [(fname[p], d_s[p], c_s[p], pure[p]) for p in comp]
     dr = res.dispatch_rows(i)
-    disp = []
-    for j in range(k):
-        p = int(dr["inv"][j])
-        disp.append(DispatchAudit(now=float(rec["dispatch"][p]), function=names[int(pt.flow[p])],
-                                  vt_before=float(dr["vt_before"][j]),
-                                  global_vt=float(dr["gvt"][j]), queue_len=int(dr["qlen"][j]),
-                                  in_flight=int(dr["inflight"][j]), device=int(rec["device"][p]),
-                                  start_state=STATE_BY_CODE[int(rec["state"][p])].value))
+    disp = [DispatchAudit(now=d_s[p], function=fname[p], vt_before=vb, global_vt=g, queue_len=q,
+                          in_flight=fl, device=dv[p], start_state=st[p])
+            for p, vb, g, q, fl in zip(dr["inv"][:k].tolist(), dr["vt_before"][:k].tolist(),
+                                        dr["gvt"][:k].tolist(), dr["qlen"][:k].tolist(),
+                                        dr["inflight"][:k].tolist())]
     audit = AuditLog(dispatches=disp, exec=exe)
     if res.cfg.outputs & _abi.WANT_AUDIT:
         rows, meta = res.util_rows(i)
-        audit.util = [(float(r[0]), int(m[0]), float(r[1]), float(r[2]), int(m[1]))
-                      for r, m in zip(rows, meta)]
+        audit.util = [(r[0], m[0], r[1], r[2], m[1]) for r, m in zip(rows.tolist(), meta.tolist())]
         bt, bm = res.backlog_rows(i)
-        audit.backlog = [(float(t), names[int(m) >> 1], bool(int(m) & 1)) for t, m in zip(bt, bm)]
+        audit.backlog = [(t, names[m >> 1], bool(m & 1)) for t, m in zip(bt.tolist(), bm.tolist())]
     return SimResult(records=records, audit=audit)
 
 
