@@ -560,7 +560,8 @@ using namespace gfq;
 
 // the k_sim instantiation of each kernel class (see gfq_prepare)
 // CTA-mode classes: 6 generic, 7 MQFQ-Sticky and 8 FCFS on a 1-device DeviceSet
-enum { NCLASS = 9, CLASS_CTA = 6, CLASS_CTA_MQFQ1 = 7, CLASS_CTA_FCFS1 = 8 };
+// class 6: MQFQ-Sticky on a 1-device DeviceSet with the audit / event / eviction logs
+enum { NCLASS = 10, CLASS_MQFQ_LOG = 6, CLASS_CTA = 7, CLASS_CTA_MQFQ1 = 8, CLASS_CTA_FCFS1 = 9 };
 static inline bool is_cta_class(int k) { return k >= CLASS_CTA; }
 static const void* class_kernel(int k, bool flows_global) {
     switch (k) {
@@ -577,6 +578,7 @@ static const void* class_kernel(int k, bool flows_global) {
                                     : (const void*)k_sim<PB_FCFS, true, false>;
         case 4: return (const void*)k_sim<PB_BATCH, true, false>;
         case 5: return (const void*)k_sim<PB_SJF, true, false>;
+        case CLASS_MQFQ_LOG: return (const void*)k_sim<PB_MQFQ_LOG, true, false>;
         default: return flows_global ? (const void*)k_sim<PB_GENERIC, false, true>
                                      : (const void*)k_sim<PB_GENERIC, false, false>;
     }
@@ -1199,6 +1201,13 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
                 if (s.policy == GFQ_POLICY_MQFQ) k = CLASS_CTA_MQFQ1;
                 else if (s.policy == GFQ_POLICY_FCFS || s.policy == GFQ_POLICY_FCFS_NAIVE) k = CLASS_CTA_FCFS1;
             }
+        } else if (logs && s.device_model == GFQ_DEVMODEL_DEVICESET) {
+            // the logs asked for (run_simulation, Simulation, the CLI): MQFQ-Sticky
+            // on one device has its own build, with the same u16 / integral rules
+            const int64_t tn = h->h_trace_off[s.trace + 1] - h->h_trace_off[s.trace];
+            if (s.policy == GFQ_POLICY_MQFQ && s.n_devices == 1 && h->h_tab_int[s.flowtab] &&
+                !L.flows_global && tn < 65535)
+                k = CLASS_MQFQ_LOG;
         } else if (!logs && s.device_model == GFQ_DEVMODEL_DEVICESET) {
             // (and, with the flow state in shared memory, u16 per-flow counters:
             // traces under 65535 arrivals)
@@ -1226,7 +1235,7 @@ int gfq_prepare(gfq_handle* h, const gfq_sim* sims, int32_t n_sims, const gfq_la
     Layout Lk[NCLASS];
     for (int k = 0; k < NCLASS; k++) Lk[k] = L;
     if (!L.cta && !L.flows_global)
-        for (int k = 2; k <= 5; k++) { Lk[k].i16 = 1; layout_finish(Lk[k]); }
+        for (int k = 2; k <= CLASS_MQFQ_LOG; k++) { Lk[k].i16 = 1; layout_finish(Lk[k]); }
     if (!L.cta && !L.flows_global && c.event_capacity <= 0) {
         const int32_t e_tok = std::max(64, (2 * R * nd + 32 + 31) & ~31);
         for (int k = 3; k <= 5; k++)

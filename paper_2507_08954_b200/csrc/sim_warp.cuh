@@ -164,7 +164,8 @@ enum { C_EVENTS = 0, C_CALLS, C_DISP, C_UTIL, C_MAXEV, C_GSCAN, C_RSCAN, C_CSCAN
 
 // Build classes: PB_GENERIC handles every policy, the scripted token provider
 // and the audit / event logs; the others are one policy on a DeviceSet.
-enum { PB_GENERIC = 0, PB_MQFQ = 1, PB_FCFS = 2, PB_BATCH = 3, PB_SJF = 4 };
+enum { PB_GENERIC = 0, PB_MQFQ = 1, PB_FCFS = 2, PB_BATCH = 3, PB_SJF = 4,
+       PB_MQFQ_LOG = 5 };   // MQFQ-Sticky on one device WITH the audit / event / eviction logs
 
 // Once per warp slice at kernel start: the arrival window's two mbarriers
 // (see WarpSim::ring_start) and their phase-parity word.
@@ -206,6 +207,11 @@ FI void cta_bar(int id, int n) { asm volatile("barrier.sync %0, %1;" ::"r"(id), 
 template <int POL, bool ND1, bool CTA = false, bool FG = false>
 struct WarpSim {
     static constexpr bool G = POL == PB_GENERIC;
+    // the build writes the logs (utilization / backlog audit, processed-event
+    // log, eviction log, per-row event indices, start tags): the generic
+    // build, and the MQFQ 1-device build the drop-ins use (run_simulation,
+    // Simulation, the CLI ask for every log)
+    static constexpr bool LG = G || POL == PB_MQFQ_LOG;
     // FG: the flow/event part lives in global scratch; its lane-strided scans
     // keep several loads in flight (a smem build keeps them rolled: its hot
     // code size is what bounds it)
@@ -299,7 +305,7 @@ struct WarpSim {
     // G = generic build (every policy, the scripted token provider, audit and
     // event logs); !G = the MQFQ-Sticky / DeviceSet build the sweeps run
 #define SCRIPTED (G && scripted_)
-#define MQFQ (G ? mqfq_ : POL == PB_MQFQ)
+#define MQFQ (G ? mqfq_ : (POL == PB_MQFQ || POL == PB_MQFQ_LOG))
 #define FCFS (G ? fcfs_ : POL == PB_FCFS)
 #define BATCH (G ? policy == GFQ_POLICY_BATCH : POL == PB_BATCH)
 #define SJF (G ? policy == GFQ_POLICY_SJF : POL == PB_SJF)
@@ -689,10 +695,10 @@ struct WarpSim {
             ust(PM(d, v), m | (1u << 27));                 // tentatively HOST_WARM
             free_mb += mem(pm_fn(m));
             nsw++;
-            if (G) evict_log(d, pm_fn(m));                 // eviction_log.append, in victim order
+            if (LG) evict_log(d, pm_fn(m));                // eviction_log.append, in victim order
         }
         bool ok = free_mb >= needed;
-        if (G && !ok) n_evict -= nsw;                      // rollback pops them (device.py:175-177)
+        if (LG && !ok) n_evict -= nsw;                     // rollback pops them (device.py:175-177)
         if (nsw) {   // commit (-> HOST_WARM) or roll back, one entry at a time
             #pragma unroll 1
             for (int base = 0; base < np; base += 32) {
@@ -1211,7 +1217,7 @@ struct WarpSim {
                 int64_t o = roff + k;
                 P.dsp_inv[o] = inv; P.dsp_vt[o] = vt_before; P.dsp_gvt[o] = g;
                 P.dsp_qlen[o] = qlen; P.dsp_infl[o] = infl_after;
-                if (G) P.dsp_ev[o] = n_events;         // Simulation.step() replay
+                if (LG) P.dsp_ev[o] = n_events;        // Simulation.step() replay
             }
             __syncwarp();                    // reconverge after the lane-0 write
         }
@@ -1295,7 +1301,7 @@ struct WarpSim {
                 u64 k = okey(v);
                 if (k < gmin) gmin = k;
             }
-            if (G && MQFQ && P.L.o_lst) {                 // FlowQueue.enqueue start tag, core.py:131-134
+            if (LG && MQFQ && P.L.o_lst) {                 // FlowQueue.enqueue start tag, core.py:131-134
                 double* lst = (double*)(fe + P.L.o_lst);
                 const double stag = pymax(lst[fn], v + (double)pe * tau()[fn]);
                 ust(lst[fn], stag);
@@ -1332,13 +1338,13 @@ struct WarpSim {
     // engine (engine.py)
 
     FI void backlog_audit(int fn, bool on) {
-        if (!G) return;
+        if (!LG) return;
         int k = n_backlog++;
-        if ((G && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_backlog_cap) {
+        if ((LG && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_backlog_cap) {
             int64_t o = (int64_t)sid * P.audit_backlog_cap + k;
             P.backlog_time[o] = now; P.backlog_meta[o] = (fn << 1) | (on ? 1 : 0);
         }
-        if (G) __syncwarp();
+        if (LG) __syncwarp();
     }
 
     // Device.eviction_log row (device.py:92): lane 0 writes (now, device, flow)
@@ -1383,7 +1389,7 @@ struct WarpSim {
     FI void swap_out_inactive() {
         if (LIKELY(!any_newly)) return;
         any_newly = false;
-        if (G && (P.outputs & GFQ_WANT_EVICTIONS)) swap_out_log();
+        if (LG && (P.outputs & GFQ_WANT_EVICTIONS)) swap_out_log();
         if (newly_n <= NEWLY_CAP) {
             // no idle container of any listed function on any device: swap_out
             // and mark_evictable change nothing, and a later unmark_evictable
@@ -1583,13 +1589,13 @@ struct WarpSim {
             if (inst != 0.0) ps_add(util_sum, inst);
             int eff = monitor_tick(d, inst, id);
             int k = n_util++;
-            if ((G && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_util_cap) {
+            if ((LG && (P.outputs & GFQ_WANT_AUDIT)) && lane == 0 && k < P.audit_util_cap) {
                 int64_t o = (int64_t)sid * P.audit_util_cap + k;
                 P.util_rows[o * 3 + 0] = now; P.util_rows[o * 3 + 1] = inst;
                 P.util_rows[o * 3 + 2] = UAVG(d);
                 P.util_meta[o * 2 + 0] = d; P.util_meta[o * 2 + 1] = eff;
             }
-            if (G) __syncwarp();
+            if (LG) __syncwarp();
         }
         if (cursor < n || tot_pend > 0 || tot_infl > 0) push_tick(now + period);
         else { tick_on = false; tick_t = __longlong_as_double(0x7ff0000000000000ll); }
@@ -1620,14 +1626,14 @@ struct WarpSim {
     }
 
     FI void log_event(double t, int kind, long long payload) {
-        if (!G) return;
+        if (!LG) return;
         int k = n_evlog++;
-        if ((G && (P.outputs & GFQ_WANT_EVENTS)) && lane == 0 && k < P.event_log_cap) {
+        if ((LG && (P.outputs & GFQ_WANT_EVENTS)) && lane == 0 && k < P.event_log_cap) {
             int64_t o = (int64_t)sid * P.event_log_cap + k;
             P.event_time[o] = t;
             P.event_meta[o] = (int64_t)((payload << 2) | kind);
         }
-        if (G) __syncwarp();
+        if (LG) __syncwarp();
     }
 
     // Simulation.run / step, engine.py:99-119
@@ -1638,7 +1644,7 @@ struct WarpSim {
         if (RING) ring_start();
         double t_arr = n > 0 ? (RING ? ring_t(0) : arr(0)) : INF;
         // trailing keep-alive expiries still log events and swap-out evictions
-        const bool early = P.early_exit && !(G && (P.outputs & (GFQ_WANT_EVENTS | GFQ_WANT_EVICTIONS)));
+        const bool early = P.early_exit && !(LG && (P.outputs & (GFQ_WANT_EVENTS | GFQ_WANT_EVICTIONS)));
         #pragma unroll 1
         for (;;) {
             if (!pmin_ok) { const long long p0 = pclk(); pool_min(); prof(PF_POOL, p0); }
