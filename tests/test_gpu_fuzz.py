@@ -1,7 +1,7 @@
 """Randomised parity: 480 random simulations (every policy; 1-3 devices;
 D, T, alpha, default TTL, pool size / disabled, dynamic D, utilisation
 threshold and window, PCIe bandwidth, prefetch overlap, interference,
-heterogeneous profiles) run as one batch and checked against the C oracle:
+heterogeneous profiles, a third of them with non-integral memory sizes) run as one batch and checked against the C oracle:
 dispatch rows and completion records bit for bit, per-function statistics
 and the run summary within 1e-9.  The batch runs through each build: the
 specialised warp classes (statistics + records + dispatch rows, early
@@ -37,8 +37,15 @@ def _workload(rng, n_sims):
         def warm_cold(p):
             w = p.warm_exec_s * float(rng.uniform(0.5, 2.0))
             return w, max(w, p.cold_exec_s * float(rng.uniform(0.5, 2.0)))
+        # a third of the tables get non-integral memory sizes: those simulations
+        # leave the 1-device fast classes (integer resident-memory sums) for
+        # the classes that replay CPython's compensated sum in pool order
+        frac = bool(rng.random() < 1 / 3)
+        def mem_mb():
+            m = float(rng.choice([256.0, 512.0, 1024.0, 1500.0, 3000.0]))
+            return m * float(rng.uniform(0.5, 1.3)) if frac else m
         profiles = {nm: FunctionProfile(nm, *warm_cold(p),
-                                        float(rng.choice([256.0, 512.0, 1024.0, 1500.0, 3000.0])),
+                                        mem_mb(),
                                         float(rng.uniform(0.1, 0.7)),
                                         float(rng.choice([1.0, 1.0, 2.0, 0.5])))
                     for nm, p in base.items()}
